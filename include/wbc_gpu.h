@@ -1,0 +1,148 @@
+/* wbc_gpu.h -- C ABI of the B200-native weighted betweenness-centrality engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   wbc::BcResult wbc::bc_parallel(const CsrGraph&, const EngineOptions&)
+ *   (/root/reference/proj/include/wbc/engine.hpp:130, src/engine.cpp:372-457).
+ * The C++ wrapper in include/wbc/engine.hpp (same signature as the reference)
+ * and the Python mirror (paper_1701_05975_b200/__init__.py) both call these
+ * entry points; INTEGRATION.md shows the binding a reference maintainer adds.
+ *
+ * Conventions: 0 = OK, negative = error (WBC_E_*); no exceptions cross the
+ * ABI; host buffers are caller-owned; the library owns device memory through
+ * the opaque handle.  wbc_gpu_last_error() returns a thread-local message for
+ * the last failing call on this thread.
+ */
+#ifndef WBC_GPU_H
+#define WBC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes.  The C++ wrapper maps WBC_E_INVALID to std::invalid_argument
+ * (the reference's exception type for bad sources / options,
+ * engine.cpp:110-114,354,373-374) and everything else to std::runtime_error. */
+#define WBC_OK 0
+#define WBC_E_INVALID (-1)     /* bad argument: source out of range, bad graph arrays */
+#define WBC_E_UNSUPPORTED (-2) /* weights not positive integers, distance bound >= 2^32 */
+#define WBC_E_CUDA (-3)        /* CUDA runtime failure (message has cudaGetErrorString) */
+#define WBC_E_NOMEM (-4)       /* device allocation failed */
+#define WBC_E_NOT_BUILT (-5)   /* library built without a usable sm_100a device */
+
+/* Flags for wbc_gpu_bc / wbc_gpu_bc_device. */
+#define WBC_HALVED 1u   /* Normalization::Halved (result.hpp:9-12): scale by 0.5 */
+#define WBC_EDGE_BC 2u  /* EngineOptions::compute_edge_bc (engine.hpp:111) */
+
+typedef struct wbc_gpu_graph wbc_gpu_graph;
+
+/* Upload an immutable CsrGraph (graph.hpp:56-69) to `device`.
+ * Replaces: the reference has no upload; bc_parallel reads CsrGraph fields
+ * directly (engine.cpp:59-212).
+ *   offsets[n+1], adjacency[2m], weights[2m], min_incident_weight[n]
+ *   (+inf for isolated vertices), edge_id[2m] (nullable: edge BC then
+ *   unavailable).  Weights must be positive integers (all reference configs
+ *   use assign_weights integers, generate.cpp:121-128) and (n-1)*max_weight
+ *   must stay below 2^32-1 so that distances are exact u32 (else
+ *   WBC_E_UNSUPPORTED).  device < 0 selects the current CUDA device. */
+int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
+                         const uint32_t* adjacency, const double* weights,
+                         const double* min_incident_weight, const uint32_t* edge_id,
+                         int device, wbc_gpu_graph** out);
+
+/* Release the handle and all device memory it owns. */
+void wbc_gpu_graph_destroy(wbc_gpu_graph* g);
+
+/* Betweenness centrality over a source list, host buffers in and out.
+ * Replaces: wbc::bc_parallel (engine.cpp:372-457) after option validation.
+ *   sources == NULL: every vertex (EngineOptions::sources unset); otherwise
+ *   the k listed sources in order, duplicates counted twice
+ *   (engine.cpp:349-361); any source >= n -> WBC_E_INVALID with the
+ *   reference's message.
+ *   node_bc[n] (required), edge_bc[m] (required iff WBC_EDGE_BC),
+ *   depth_per_source[n] (nullable; settlement rounds of each run source,
+ *   0 otherwise -- result.hpp:19-22), elapsed_s (nullable; wall time from
+ *   after validation to after normalization, like BcResult::elapsed,
+ *   engine.cpp:375,455). */
+int wbc_gpu_bc(wbc_gpu_graph* g, const uint32_t* sources, uint64_t k, uint32_t flags,
+               double* node_bc, double* edge_bc, uint32_t* depth_per_source,
+               double* elapsed_s);
+
+/* Same computation with device-resident buffers on a caller stream
+ * (cudaStream_t passed as void*; NULL = legacy default stream).  Outputs are
+ * ACCUMULATED into d_node_bc / d_edge_bc (caller zeroes them), which is what
+ * a multi-rank run needs before its one allreduce; depth entries of run
+ * sources are overwritten.  Normalization is applied only if WBC_HALVED is
+ * set.  Asynchronous: returns after enqueueing.  Sources are NOT range
+ * checked on the device path (caller validated them). */
+int wbc_gpu_bc_device(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k,
+                      uint32_t flags, double* d_node_bc, double* d_edge_bc,
+                      uint32_t* d_depth_per_source, void* stream);
+
+/* Parity/debug: one source's final traversal state, host buffers.
+ * Replaces: solve_source + accumulate_dependencies (engine.hpp:93-99,
+ * engine.cpp:183-222).  dist[n] (+inf unreachable), sigma[n], delta[n]
+ * (nullable each), depth (nullable). */
+int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* sigma,
+                      double* delta, uint32_t* depth);
+
+/* Introspection for benches/tests.  Any pointer may be NULL. */
+int wbc_gpu_graph_info(wbc_gpu_graph* g, uint32_t* n, uint32_t* m, uint32_t* max_weight,
+                       int* packed_slots, uint32_t* near_width, uint64_t* graph_bytes);
+
+/* Tuning knobs (0 = automatic): threads per CTA (128/256/512), resident
+ * source slots (CTAs), near-window width of the pending split. */
+int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
+                       uint32_t near_width);
+
+/* Counters of the last run: [0]=slots used, [1]=threads per CTA,
+ * [2]=sources that overflowed the DAG-edge buffer (row-scan fallback),
+ * [3]=kernel launches issued by the last wbc_gpu_bc* call. */
+int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4);
+
+const char* wbc_gpu_last_error(void);
+
+/* ---- host-side helpers (the CSR loader and generators of the reference,
+ * re-implemented natively with identical output; exported for bindings) ---- */
+
+typedef struct wbc_edge_list wbc_edge_list;
+typedef struct wbc_csr wbc_csr;
+
+/* parse_edge_list (graph.hpp:47): text in, edge list out.  On ParseError
+ * returns WBC_E_PARSE and *err_line = the 1-based line. */
+#define WBC_E_PARSE (-6)
+int wbc_host_parse_edge_list(const char* text, size_t len, double default_weight,
+                             wbc_edge_list** out, uint64_t* err_line);
+wbc_edge_list* wbc_host_edges_new(uint64_t len, const uint64_t* u, const uint64_t* v,
+                                  const double* w);
+uint64_t wbc_host_edges_len(const wbc_edge_list* e);
+uint64_t wbc_host_edges_self_loops(const wbc_edge_list* e);
+void wbc_host_edges_get(const wbc_edge_list* e, uint64_t* u, uint64_t* v, double* w);
+void wbc_host_edges_free(wbc_edge_list* e);
+
+/* Generators (generate.hpp:20-35) with the reference's exact output streams,
+ * plus two configs the reference lacks: Barabasi-Albert and a
+ * row-major 4-neighbour grid.  Weights are 1 until wbc_host_assign_weights. */
+int wbc_host_gen_er(uint64_t n, double avg_degree, uint64_t seed, wbc_edge_list** out);
+int wbc_host_gen_kronecker(int scale, double avg_degree, uint64_t seed, wbc_edge_list** out);
+int wbc_host_gen_ba(uint64_t n, uint32_t m_per_node, uint64_t seed, wbc_edge_list** out);
+int wbc_host_gen_grid(uint32_t rows, uint32_t cols, wbc_edge_list** out);
+int wbc_host_assign_weights(wbc_edge_list* e, int lo, int hi, uint64_t seed);
+int wbc_host_sample_sources(uint32_t n, uint32_t k, uint64_t seed, uint32_t* out,
+                            uint32_t* out_len);
+
+/* build_csr (graph.hpp:74): identical CsrGraph arrays. */
+int wbc_host_build_csr(const wbc_edge_list* e, wbc_csr** out);
+void wbc_host_csr_dims(const wbc_csr* g, uint32_t* n, uint32_t* m, uint64_t* merged);
+void wbc_host_csr_get(const wbc_csr* g, uint32_t* offsets, uint32_t* adjacency,
+                      double* weights, uint32_t* edge_id, double* min_incident_weight,
+                      uint64_t* original_id, uint32_t* edge_u, uint32_t* edge_v);
+void wbc_host_csr_free(wbc_csr* g);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WBC_GPU_H */

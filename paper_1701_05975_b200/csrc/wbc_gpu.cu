@@ -1,0 +1,517 @@
+// wbc_gpu.cu -- the C ABI (include/wbc_gpu.h) over the sm_100a kernels.
+//
+// Owns the device CSR replica and the per-slot workspaces; validates the
+// reference's argument contract (engine.cpp:349-361,372-385) at the boundary;
+// launches the persistent per-source kernel (bc_kernels.cuh) on the caller's
+// stream.  No CPU fallback exists: without a device every entry point fails
+// with WBC_E_CUDA / WBC_E_NOT_BUILT.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bc_kernels.cuh"
+#include "wbc_gpu.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define WBC_CUDA_TRY(expr)                                                                  \
+  do {                                                                                      \
+    const cudaError_t err_ = (expr);                                                        \
+    if (err_ != cudaSuccess)                                                                \
+      return set_error(err_ == cudaErrorMemoryAllocation ? WBC_E_NOMEM : WBC_E_CUDA,        \
+                       std::string(#expr) + ": " + cudaGetErrorString(err_));               \
+  } while (0)
+
+template <class T>
+T* dev_alloc(size_t count, cudaError_t& err) {
+  void* p = nullptr;
+  err = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+  return static_cast<T*>(p);
+}
+
+uint32_t bits_for(uint64_t x) {  // bits needed to store values 0..x
+  uint32_t b = 1;
+  while (b < 64 && (x >> b) != 0) ++b;
+  return b;
+}
+
+}  // namespace
+
+namespace wbc_host {
+// The host layer (host_capi.cpp) reports through the same thread-local slot.
+int set_error(int code, const std::string& msg) { return ::set_error(code, msg); }
+}  // namespace wbc_host
+
+struct wbc_gpu_graph {
+  int device = 0;
+  uint32_t n = 0, m = 0;
+  uint32_t max_weight = 0;
+  bool packed = true;
+  uint32_t wbits = 0;
+  uint32_t near_width = 1;
+  int sm_count = 0;
+  // device CSR replica
+  uint32_t* d_offsets = nullptr;
+  uint32_t* d_slots32 = nullptr;
+  uint2* d_slots64 = nullptr;
+  uint32_t* d_minw = nullptr;
+  uint32_t* d_edge_id = nullptr;
+  uint64_t graph_bytes = 0;
+  // workspace
+  int ws_slots = 0;
+  int ws_threads = 0;
+  void* d_ws = nullptr;
+  wbc_dev::Workspace ws{};
+  unsigned long long* d_counter = nullptr;
+  unsigned int* d_overflow = nullptr;
+  // scratch for host-buffer runs
+  double* d_node = nullptr;
+  double* d_edge = nullptr;
+  uint32_t* d_depth = nullptr;
+  uint32_t* d_sources = nullptr;
+  uint64_t d_sources_cap = 0;
+  // tuning
+  int tune_threads = 0;
+  int tune_slots = 0;
+  uint64_t stats[4] = {0, 0, 0, 0};
+
+  ~wbc_gpu_graph() {
+    cudaSetDevice(device);
+    cudaFree(d_offsets);
+    cudaFree(d_slots32);
+    cudaFree(d_slots64);
+    cudaFree(d_minw);
+    cudaFree(d_edge_id);
+    cudaFree(d_ws);
+    cudaFree(d_counter);
+    cudaFree(d_overflow);
+    cudaFree(d_node);
+    cudaFree(d_edge);
+    cudaFree(d_depth);
+    cudaFree(d_sources);
+  }
+};
+
+namespace {
+
+using KernelFn = void (*)(const wbc_dev::RunParams);
+
+KernelFn pick_kernel(int threads, bool packed) {
+  using namespace wbc_dev;
+  if (packed) {
+    if (threads <= 128) return bc_sources_kernel<128, true>;
+    if (threads <= 256) return bc_sources_kernel<256, true>;
+    return bc_sources_kernel<512, true>;
+  }
+  if (threads <= 128) return bc_sources_kernel<128, false>;
+  if (threads <= 256) return bc_sources_kernel<256, false>;
+  return bc_sources_kernel<512, false>;
+}
+
+int auto_threads(const wbc_gpu_graph* g) {
+  if (g->tune_threads) return g->tune_threads <= 128 ? 128 : (g->tune_threads <= 256 ? 256 : 512);
+  // Small frontiers (low average degree, small n) waste wide CTAs.
+  const double avg_deg = g->n ? 2.0 * g->m / g->n : 0.0;
+  if (g->n < 16384 || avg_deg < 6.0) return 128;
+  return 256;
+}
+
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+// Ensure a workspace for `want` slots with `threads` per CTA exists.
+int ensure_workspace(wbc_gpu_graph* g, int want, int threads) {
+  const uint64_t ns = round_up(uint64_t{g->n} + 2, 64);
+  const uint64_t dag_cap = round_up(uint64_t{g->n} + uint64_t{g->n} / 2 + 1024, 64);
+  const uint64_t per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + dag_cap * 8;
+  // occupancy cap
+  int per_sm = 0;
+  WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, reinterpret_cast<const void*>(pick_kernel(threads, g->packed)), threads, 0));
+  int slots = std::max(1, per_sm) * g->sm_count;
+  if (g->tune_slots) slots = std::min(slots, g->tune_slots);
+  slots = std::min(slots, want);
+  // memory cap: keep 4 GiB + 10% headroom
+  size_t free_b = 0, total_b = 0;
+  WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  uint64_t avail = free_b + (g->d_ws ? uint64_t(g->ws_slots) * per_slot : 0);
+  const uint64_t reserve = (4ULL << 30) + total_b / 10;
+  avail = avail > reserve ? avail - reserve : 0;
+  slots = static_cast<int>(std::min<uint64_t>(slots, std::max<uint64_t>(1, avail / per_slot)));
+  if (g->d_ws && g->ws_slots >= slots && g->ws_threads == threads) return WBC_OK;
+  if (g->d_ws && g->ws_slots >= slots) {
+    g->ws_threads = threads;
+    return WBC_OK;
+  }
+  cudaFree(g->d_ws);
+  g->d_ws = nullptr;
+  void* base = nullptr;
+  const cudaError_t err = cudaMalloc(&base, per_slot * slots);
+  if (err != cudaSuccess)
+    return set_error(WBC_E_NOMEM, "workspace allocation of " + std::to_string(per_slot * slots) +
+                                      " bytes failed: " + cudaGetErrorString(err));
+  g->d_ws = base;
+  g->ws_slots = slots;
+  g->ws_threads = threads;
+  char* p = static_cast<char*>(base);
+  auto carve = [&](uint64_t bytes) {
+    char* q = p;
+    p += bytes * slots;
+    return q;
+  };
+  g->ws.n_stride = ns;
+  g->ws.dag_cap = dag_cap;
+  g->ws.sigma = reinterpret_cast<double*>(carve(ns * 8));
+  g->ws.delta = reinterpret_cast<double*>(carve(ns * 8));
+  g->ws.dag = reinterpret_cast<uint2*>(carve(dag_cap * 8));
+  g->ws.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  g->ws.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  g->ws.level_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  g->ws.near_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  g->ws.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  g->ws.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  return WBC_OK;
+}
+
+// Enqueue one run: d_sources may be null (all vertices).  Accumulates.
+int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edge_bc,
+               double* d_node, double* d_edge, uint32_t* d_depth, cudaStream_t stream,
+               bool single_slot) {
+  g->stats[3] = 0;
+  if (k == 0 || g->n == 0) return WBC_OK;
+  const int threads = auto_threads(g);
+  const int want = single_slot ? 1 : static_cast<int>(std::min<uint64_t>(k, 1u << 30));
+  int rc = ensure_workspace(g, want, threads);
+  if (rc) return rc;
+  const int slots = single_slot ? 1 : static_cast<int>(std::min<uint64_t>(g->ws_slots, k));
+  wbc_dev::RunParams p{};
+  p.g.n = g->n;
+  p.g.m = g->m;
+  p.g.offsets = g->d_offsets;
+  p.g.slots32 = g->d_slots32;
+  p.g.slots64 = g->d_slots64;
+  p.g.minw = g->d_minw;
+  p.g.edge_id = g->d_edge_id;
+  p.g.wbits = g->wbits;
+  p.g.wmask = g->wbits >= 32 ? 0xFFFFFFFFu : ((1u << g->wbits) - 1);
+  p.ws = g->ws;
+  p.sources = d_sources;
+  p.k = k;
+  p.counter = g->d_counter;
+  p.node_bc = d_node;
+  p.edge_bc = edge_bc ? d_edge : nullptr;
+  p.depth = d_depth;
+  p.near_width = g->near_width;
+  p.overflow = g->d_overflow;
+  WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter, 0, sizeof(unsigned long long), stream));
+  WBC_CUDA_TRY(cudaMemsetAsync(g->d_overflow, 0, sizeof(unsigned int), stream));
+  pick_kernel(threads, g->packed)<<<slots, threads, 0, stream>>>(p);
+  WBC_CUDA_TRY(cudaGetLastError());
+  g->stats[0] = slots;
+  g->stats[1] = threads;
+  g->stats[3] = 1;
+  return WBC_OK;
+}
+
+int scale_async(double* x, uint64_t len, double f, cudaStream_t stream) {
+  if (!len) return WBC_OK;
+  const int blocks = static_cast<int>(std::min<uint64_t>((len + 255) / 256, 4096));
+  wbc_dev::scale_kernel<<<blocks, 256, 0, stream>>>(x, len, f);
+  WBC_CUDA_TRY(cudaGetLastError());
+  return WBC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wbc_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
+                         const uint32_t* adjacency, const double* weights,
+                         const double* min_incident_weight, const uint32_t* edge_id, int device,
+                         wbc_gpu_graph** out) {
+  if (!out) return set_error(WBC_E_INVALID, "out is null");
+  *out = nullptr;
+  const uint64_t slots = 2ULL * m;
+  if (slots >= (1ULL << 32)) return set_error(WBC_E_UNSUPPORTED, "2m must fit in u32 slots");
+  if (n > 0 && (!offsets || !min_incident_weight))
+    return set_error(WBC_E_INVALID, "offsets / min_incident_weight are required");
+  if (slots > 0 && (!adjacency || !weights))
+    return set_error(WBC_E_INVALID, "adjacency / weights are required");
+  if (n > 0 && (offsets[0] != 0 || offsets[n] != slots))
+    return set_error(WBC_E_INVALID, "offsets must start at 0 and end at 2m");
+  for (uint32_t v = 0; v < n; ++v)
+    if (offsets[v + 1] < offsets[v]) return set_error(WBC_E_INVALID, "offsets not monotone");
+  uint64_t maxw = 0;
+  for (uint64_t e = 0; e < slots; ++e) {
+    const double w = weights[e];
+    if (adjacency[e] >= n) return set_error(WBC_E_INVALID, "adjacency entry out of range");
+    if (!(w >= 1.0) || w != std::floor(w) || w > 4294967295.0)
+      return set_error(WBC_E_UNSUPPORTED,
+                       "weights must be positive integers (exact u32 distances); got " +
+                           std::to_string(w));
+    maxw = std::max<uint64_t>(maxw, static_cast<uint64_t>(w));
+  }
+  if (n > 0 && uint64_t{n} * std::max<uint64_t>(maxw, 1) >= 0xFFFFFFFFULL)
+    return set_error(WBC_E_UNSUPPORTED, "n * max_weight must stay below 2^32-1");
+
+  auto g = new wbc_gpu_graph();
+  int dev = device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      delete g;
+      return set_error(WBC_E_NOT_BUILT, "no CUDA device available");
+    }
+  }
+  g->device = dev;
+  cudaError_t err = cudaSetDevice(dev);
+  if (err != cudaSuccess) {
+    delete g;
+    return set_error(WBC_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(err));
+  }
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  if (major < 10) {
+    delete g;
+    return set_error(WBC_E_NOT_BUILT, "device is not sm_100 class (built for sm_100a only)");
+  }
+  g->n = n;
+  g->m = m;
+  g->max_weight = static_cast<uint32_t>(maxw);
+  g->wbits = bits_for(std::max<uint64_t>(maxw, 1));
+  const uint32_t nbits = bits_for(n ? n - 1 : 0);
+  g->packed = (g->wbits + nbits) <= 32;
+
+  // Host-side packing of the device CSR replica.
+  std::vector<uint32_t> minw(n);
+  double sum_minw = 0;
+  uint64_t cnt_minw = 0;
+  for (uint32_t v = 0; v < n; ++v) {
+    const double x = min_incident_weight[v];
+    if (std::isinf(x) || offsets[v + 1] == offsets[v]) {
+      minw[v] = wbc_dev::kInfDist;
+    } else {
+      minw[v] = static_cast<uint32_t>(x);
+      sum_minw += x;
+      ++cnt_minw;
+    }
+  }
+  // Near-window width: about half the mean minimum incident weight balances
+  // near rescans against far refills (SURVEY-style sizing in DESIGN.md).
+  g->near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 2.0 + 0.5))
+                           : 1;
+
+  g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
+  if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);
+  if (err == cudaSuccess) g->d_counter = dev_alloc<unsigned long long>(1, err);
+  if (err == cudaSuccess) g->d_overflow = dev_alloc<unsigned int>(1, err);
+  if (err == cudaSuccess) {
+    if (g->packed) {
+      g->d_slots32 = dev_alloc<uint32_t>(slots, err);
+    } else {
+      g->d_slots64 = dev_alloc<uint2>(slots, err);
+    }
+  }
+  if (err == cudaSuccess && edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
+  if (err != cudaSuccess) {
+    delete g;
+    return set_error(WBC_E_NOMEM, std::string("graph upload: ") + cudaGetErrorString(err));
+  }
+  if (n) {
+    err = cudaMemcpy(g->d_offsets, offsets, (uint64_t{n} + 1) * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_minw, minw.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+  }
+  if (err == cudaSuccess && slots) {
+    if (g->packed) {
+      std::vector<uint32_t> packed(slots);
+      for (uint64_t e = 0; e < slots; ++e)
+        packed[e] = (adjacency[e] << g->wbits) | static_cast<uint32_t>(weights[e]);
+      err = cudaMemcpy(g->d_slots32, packed.data(), slots * 4, cudaMemcpyHostToDevice);
+    } else {
+      std::vector<uint2> wide(slots);
+      for (uint64_t e = 0; e < slots; ++e)
+        wide[e] = make_uint2(adjacency[e], static_cast<uint32_t>(weights[e]));
+      err = cudaMemcpy(g->d_slots64, wide.data(), slots * 8, cudaMemcpyHostToDevice);
+    }
+    if (err == cudaSuccess && edge_id)
+      err = cudaMemcpy(g->d_edge_id, edge_id, slots * 4, cudaMemcpyHostToDevice);
+  }
+  if (err != cudaSuccess) {
+    delete g;
+    return set_error(WBC_E_CUDA, std::string("graph upload: ") + cudaGetErrorString(err));
+  }
+  g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 4 + slots * (g->packed ? 4 : 8) +
+                   (edge_id ? slots * 4 : 0);
+  *out = g;
+  return WBC_OK;
+}
+
+void wbc_gpu_graph_destroy(wbc_gpu_graph* g) { delete g; }
+
+int wbc_gpu_graph_info(wbc_gpu_graph* g, uint32_t* n, uint32_t* m, uint32_t* max_weight,
+                       int* packed_slots, uint32_t* near_width, uint64_t* graph_bytes) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  if (n) *n = g->n;
+  if (m) *m = g->m;
+  if (max_weight) *max_weight = g->max_weight;
+  if (packed_slots) *packed_slots = g->packed ? 1 : 0;
+  if (near_width) *near_width = g->near_width;
+  if (graph_bytes) *graph_bytes = g->graph_bytes;
+  return WBC_OK;
+}
+
+int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uint32_t near_width) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  if (threads_per_cta < 0 || max_slots < 0) return set_error(WBC_E_INVALID, "negative tuning value");
+  g->tune_threads = threads_per_cta;
+  g->tune_slots = max_slots;
+  if (near_width) g->near_width = near_width;
+  if (g->d_ws && max_slots && g->ws_slots > max_slots) {
+    // shrink lazily: next run re-carves with fewer slots
+    cudaSetDevice(g->device);
+    cudaFree(g->d_ws);
+    g->d_ws = nullptr;
+    g->ws_slots = 0;
+  }
+  return WBC_OK;
+}
+
+int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4) {
+  if (!g || !stats4) return set_error(WBC_E_INVALID, "null argument");
+  std::memcpy(stats4, g->stats, sizeof g->stats);
+  return WBC_OK;
+}
+
+int wbc_gpu_bc_device(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, uint32_t flags,
+                      double* d_node_bc, double* d_edge_bc, uint32_t* d_depth_per_source,
+                      void* stream) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  if (!d_node_bc && g->n) return set_error(WBC_E_INVALID, "node_bc is required");
+  const bool edge = flags & WBC_EDGE_BC;
+  if (edge && !g->d_edge_id)
+    return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
+  if (edge && !d_edge_bc && g->m) return set_error(WBC_E_INVALID, "edge_bc is required");
+  WBC_CUDA_TRY(cudaSetDevice(g->device));
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const uint64_t kk = d_sources ? k : g->n;
+  int rc = launch_run(g, d_sources, kk, edge, d_node_bc, d_edge_bc, d_depth_per_source, st, false);
+  if (rc) return rc;
+  if (flags & WBC_HALVED) {
+    if ((rc = scale_async(d_node_bc, g->n, 0.5, st))) return rc;
+    if (edge && (rc = scale_async(d_edge_bc, g->m, 0.5, st))) return rc;
+  }
+  return WBC_OK;
+}
+
+int wbc_gpu_bc(wbc_gpu_graph* g, const uint32_t* sources, uint64_t k, uint32_t flags,
+               double* node_bc, double* edge_bc, uint32_t* depth_per_source, double* elapsed_s) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  const bool edge = flags & WBC_EDGE_BC;
+  if (!node_bc && g->n) return set_error(WBC_E_INVALID, "node_bc is required");
+  if (edge && !edge_bc && g->m) return set_error(WBC_E_INVALID, "edge_bc is required");
+  if (edge && !g->d_edge_id)
+    return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
+  if (sources)  // resolve_sources (engine.cpp:349-361)
+    for (uint64_t i = 0; i < k; ++i)
+      if (sources[i] >= g->n)
+        return set_error(WBC_E_INVALID, "bc_parallel: source id out of range");
+  const auto t0 = std::chrono::steady_clock::now();
+  WBC_CUDA_TRY(cudaSetDevice(g->device));
+  cudaError_t err = cudaSuccess;
+  if (!g->d_node) g->d_node = dev_alloc<double>(g->n, err);
+  if (err == cudaSuccess && !g->d_depth) g->d_depth = dev_alloc<uint32_t>(g->n, err);
+  if (err == cudaSuccess && edge && !g->d_edge) g->d_edge = dev_alloc<double>(g->m, err);
+  if (err != cudaSuccess) return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
+  const cudaStream_t st = 0;
+  const uint64_t kk = sources ? k : g->n;
+  if (sources && k > g->d_sources_cap) {
+    cudaFree(g->d_sources);
+    g->d_sources = dev_alloc<uint32_t>(k, err);
+    if (err != cudaSuccess) {
+      g->d_sources_cap = 0;
+      return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
+    }
+    g->d_sources_cap = k;
+  }
+  if (sources && k)
+    WBC_CUDA_TRY(cudaMemcpyAsync(g->d_sources, sources, k * 4, cudaMemcpyHostToDevice, st));
+  if (g->n) {
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_node, 0, uint64_t{g->n} * 8, st));
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_depth, 0, uint64_t{g->n} * 4, st));
+  }
+  if (edge && g->m) WBC_CUDA_TRY(cudaMemsetAsync(g->d_edge, 0, uint64_t{g->m} * 8, st));
+  int rc = launch_run(g, sources ? g->d_sources : nullptr, kk, edge, g->d_node, g->d_edge,
+                      g->d_depth, st, false);
+  if (rc) return rc;
+  if (flags & WBC_HALVED) {  // engine.cpp:451-454
+    if ((rc = scale_async(g->d_node, g->n, 0.5, st))) return rc;
+    if (edge && (rc = scale_async(g->d_edge, g->m, 0.5, st))) return rc;
+  }
+  if (g->n) {
+    WBC_CUDA_TRY(cudaMemcpyAsync(node_bc, g->d_node, uint64_t{g->n} * 8, cudaMemcpyDeviceToHost, st));
+    if (depth_per_source)
+      WBC_CUDA_TRY(cudaMemcpyAsync(depth_per_source, g->d_depth, uint64_t{g->n} * 4,
+                                   cudaMemcpyDeviceToHost, st));
+  }
+  if (edge && g->m)
+    WBC_CUDA_TRY(cudaMemcpyAsync(edge_bc, g->d_edge, uint64_t{g->m} * 8, cudaMemcpyDeviceToHost, st));
+  unsigned int overflow = 0;
+  WBC_CUDA_TRY(cudaMemcpyAsync(&overflow, g->d_overflow, 4, cudaMemcpyDeviceToHost, st));
+  WBC_CUDA_TRY(cudaStreamSynchronize(st));
+  g->stats[2] = kk ? overflow : 0;
+  if (elapsed_s)
+    *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return WBC_OK;
+}
+
+int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* sigma,
+                      double* delta, uint32_t* depth) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  if (source >= g->n) return set_error(WBC_E_INVALID, "init_state: source out of range");
+  WBC_CUDA_TRY(cudaSetDevice(g->device));
+  const int threads = auto_threads(g);
+  int rc = ensure_workspace(g, 1, threads);
+  if (rc) return rc;
+  cudaError_t err = cudaSuccess;
+  double* d_scratch = dev_alloc<double>(g->n, err);
+  uint32_t* d_src = dev_alloc<uint32_t>(1, err);
+  uint32_t* d_dep = dev_alloc<uint32_t>(g->n, err);
+  if (err != cudaSuccess) return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
+  const uint64_t n = g->n;
+  WBC_CUDA_TRY(cudaMemcpy(d_src, &source, 4, cudaMemcpyHostToDevice));
+  WBC_CUDA_TRY(cudaMemset(d_scratch, 0, n * 8));
+  WBC_CUDA_TRY(cudaMemset(d_dep, 0, n * 4));
+  WBC_CUDA_TRY(cudaMemset(g->ws.sigma, 0, n * 8));  // slot 0: unreached stay 0
+  WBC_CUDA_TRY(cudaMemset(g->ws.delta, 0, n * 8));
+  rc = launch_run(g, d_src, 1, false, d_scratch, nullptr, d_dep, 0, true);
+  if (rc) return rc;
+  WBC_CUDA_TRY(cudaDeviceSynchronize());
+  std::vector<uint32_t> du(n);
+  WBC_CUDA_TRY(cudaMemcpy(du.data(), g->ws.dist, n * 4, cudaMemcpyDeviceToHost));
+  if (dist)
+    for (uint64_t i = 0; i < n; ++i)
+      dist[i] = du[i] == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(du[i]);
+  if (sigma) WBC_CUDA_TRY(cudaMemcpy(sigma, g->ws.sigma, n * 8, cudaMemcpyDeviceToHost));
+  if (delta) WBC_CUDA_TRY(cudaMemcpy(delta, g->ws.delta, n * 8, cudaMemcpyDeviceToHost));
+  if (depth) WBC_CUDA_TRY(cudaMemcpy(depth, d_dep + source, 4, cudaMemcpyDeviceToHost));
+  cudaFree(d_scratch);
+  cudaFree(d_src);
+  cudaFree(d_dep);
+  return WBC_OK;
+}
+
+}  // extern "C"

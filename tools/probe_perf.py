@@ -1,0 +1,34 @@
+"""Dev probe: quick GPU timing of the BC path on a named config (not the bench)."""
+import argparse, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_1701_05975_b200 as W
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--graph", default="rmat20")
+ap.add_argument("--k", type=int, default=256)
+ap.add_argument("--threads", type=int, default=0)
+ap.add_argument("--slots", type=int, default=0)
+ap.add_argument("--near", type=int, default=0)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+t = time.time()
+if a.graph.startswith("rmat"):
+    el = W.assign_weights(W.gen_kronecker(int(a.graph[4:]), 32.0, 1), 1, 255, 1)
+elif a.graph == "er":
+    el = W.assign_weights(W.gen_er(4096, 8.0, 1), 1, 64, 1)
+elif a.graph == "ba":
+    el = W.assign_weights(W.gen_ba(65536, 10, 1), 1, 100, 1)
+elif a.graph.startswith("grid"):
+    s = int(a.graph[4:]); el = W.assign_weights(W.gen_grid(s, s), 1, 1000, 1)
+g = W.build_csr(el)
+print(f"graph {a.graph} n={g.n} m={g.m} built in {time.time()-t:.1f}s", flush=True)
+gg = W.GpuGraph(g, 0)
+gg.set_tuning(a.threads, a.slots, a.near)
+print(gg.info(), flush=True)
+src = W.sample_sources(g.n, a.k, 1)
+for rep in range(a.reps):
+    r = gg.bc(W.EngineOptions(sources=src))
+    st = gg.last_run_stats()
+    print(f"rep {rep}: {r.elapsed*1e3:.1f} ms for {len(src)} sources -> {g.m*len(src)/r.elapsed/1e9:.2f} GTEPS; "
+          f"{r.elapsed/len(src)*1e3:.3f} ms/src; stats {st}; depth mean {r.depth_per_source[src].mean():.1f}", flush=True)
