@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Weighted-BC throughput bench (BASELINE.json metric: GTEPS = m x sources / s).
+
+Default workload: BASELINE config 3, R-MAT scale 20 edgefactor 16 (gen_kronecker
+(20, 32, 1)), integer weights 1-255 (assign_weights seed 1), 4096 sources from
+sample_sources(n, 4096, 1).  One step = the BC of the whole 4096-source sample
+(sources strided across ranks, one NCCL allreduce of the partial BC when N > 1:
+strong scaling).  Other configs: --workload er4096 | ba65536 | grid2048 | rmat20.
+
+  python bench.py [--gpus N --steps K --warmup W]      # our GPU arm
+  python bench.py --impl reference                      # the reference's CPU bc_parallel
+
+The JSON line carries: value (device-timed, inputs resident), e2e (through the
+host-buffer C ABI wbc_gpu_bc, H2D sources + D2H results inside the timing),
+roofline of the BC kernel (algorithmic bytes 72m+88n per source, SURVEY.md §8d,
+over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs),
+cpu_baseline (the compiled reference on this host's cores, bounded sample),
+clocks sampled during the timed region and gpu_launches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "weighted-BC GTEPS (m×sources/s) at 1/2/4/8 B200; speedup vs CPU Brandes"
+
+WORKLOADS = {
+    # name: (builder description, sources (None = all), weights)
+    "er4096": dict(kind="er", n=4096, deg=8.0, lo=1, hi=64, sources=None),
+    "ba65536": dict(kind="ba", n=65536, mper=10, lo=1, hi=100, sources=None),
+    "rmat20": dict(kind="rmat", scale=20, deg=32.0, lo=1, hi=255, sources=4096),
+    "grid2048": dict(kind="grid", side=2048, lo=1, hi=1000, sources=1024),
+    "rmat24": dict(kind="rmat", scale=24, deg=32.0, lo=1, hi=255, sources=65536),
+}
+
+
+# The reference's fastest bc_parallel schedule per family.
+BEST_STRATEGY = {"er": "np", "ba": "we-warp32", "rmat": "we", "grid": "we"}
+
+
+def describe(wl: dict) -> str:
+    k = wl["kind"]
+    if k == "er":
+        return f"gen_er({wl['n']},{wl['deg']},1)+assign_weights({wl['lo']},{wl['hi']},1)"
+    if k == "ba":
+        return f"gen_ba({wl['n']},{wl['mper']},1)+assign_weights({wl['lo']},{wl['hi']},1)"
+    if k == "rmat":
+        return f"gen_kronecker({wl['scale']},{wl['deg']},1)+assign_weights({wl['lo']},{wl['hi']},1)"
+    return f"gen_grid({wl['side']},{wl['side']})+assign_weights({wl['lo']},{wl['hi']},1)"
+
+
+def build_graph_ours(wl):
+    import paper_1701_05975_b200 as W
+    k = wl["kind"]
+    if k == "er":
+        el = W.gen_er(wl["n"], wl["deg"], 1)
+    elif k == "ba":
+        el = W.gen_ba(wl["n"], wl["mper"], 1)
+    elif k == "rmat":
+        el = W.gen_kronecker(wl["scale"], wl["deg"], 1)
+    else:
+        el = W.gen_grid(wl["side"], wl["side"])
+    el = W.assign_weights(el, wl["lo"], wl["hi"], 1)
+    g = W.build_csr(el)
+    src = W.sample_sources(g.n, wl["sources"], 1) if wl["sources"] else np.arange(g.n, dtype=np.uint32)
+    return el, g, src
+
+
+def algorithmic_bytes_per_source(n: int, m: int) -> int:
+    """B_src = 72 m + 88 n."""
+    return 72 * m + 88 * n
+
+
+def load_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload: str):
+    """dram bytes per source of the BC kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(workload)
+    return None if e is None else float(e["dram_bytes_per_source"])
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.tmp.flush()
+        self.tmp.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.tmp.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.tmp.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(wl_name: str, wl: dict, target_s: float = 15.0):
+    """The compiled reference (oracle/_ref) bc_parallel on this host, bounded sample."""
+    from oracle import REF_SO, Oracle, RefLib
+    cores = os.cpu_count() or 1
+    if os.path.exists(REF_SO):
+        R = RefLib()
+        g, src_all = build_graph_ref(R, wl)
+        kind = "reference"
+        strategy = BEST_STRATEGY[wl["kind"]]
+
+        def run(src):
+            t = time.perf_counter()
+            R.bc_parallel(g, strategy, cores, sources=src)
+            return time.perf_counter() - t
+    else:  # port: the plain-C oracle, single-threaded
+        import paper_1701_05975_b200 as W  # graph arrays only; the timed code is the oracle
+        _, g, src_all = build_graph_ours(wl)
+        O = Oracle()
+        kind = "port"
+        cores = 1
+        strategy = "eq4 (oracle)"
+
+        def run(src):
+            t = time.perf_counter()
+            O.bc_eq4(g, sources=src)
+            return time.perf_counter() - t
+    # calibrate on a small batch, then size the sample to ~target_s
+    probe = src_all[: max(1, min(len(src_all), cores))]
+    t_probe = run(probe)
+    per_src = t_probe / len(probe)
+    k = int(max(len(probe), min(len(src_all), target_s / max(per_src, 1e-9))))
+    k = max(k - k % max(1, min(cores, k)), len(probe)) if kind == "reference" else k
+    sample = src_all[:k]
+    t = run(sample)
+    value = g.m * len(sample) / t / 1e9
+    if kind == "reference":
+        R.free_csr(g)
+    return dict(value=value, unit="GTEPS", cores=cores, kind=kind,
+                sample=f"first {len(sample)} of the {wl_name} source list, bc_parallel strategy={strategy} "
+                       f"workers={cores}, {t:.2f}s wall" if kind == "reference" else
+                       f"first {len(sample)} sources, oracle bc_eq4 single-thread, {t:.2f}s")
+
+
+def build_graph_ref(R, wl):
+    k = wl["kind"]
+    if k == "er":
+        u, v, w = R.gen_er(wl["n"], wl["deg"], 1)
+    elif k == "rmat":
+        u, v, w = R.gen_kronecker(wl["scale"], wl["deg"], 1)
+    else:  # no reference generator for BA / grid: our generator's edge list, reference CSR + engine
+        el, _, _ = build_graph_ours(wl)
+        u, v, w = el.u, el.v, el.w
+    if k in ("er", "rmat"):
+        u, v, w = R.assign_weights(u, v, w, wl["lo"], wl["hi"], 1)
+    g = R.build_csr(u, v, w)
+    src = R.sample_sources(g.n, wl["sources"], 1) if wl["sources"] else np.arange(g.n, dtype=np.uint32)
+    return g, src
+
+
+def run_reference_arm(args, wl_name, wl):
+    """--impl reference: the reference's own CPU bc_parallel, all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import REF_SO, Oracle, RefLib
+    cores = os.cpu_count() or 1
+    if os.path.exists(REF_SO):
+        R = RefLib()
+        g, src_all = build_graph_ref(R, wl)
+        kind = "reference"
+        strategy = BEST_STRATEGY[wl["kind"]]
+        step = lambda src: R.bc_parallel(g, strategy, cores, sources=src)  # noqa: E731
+    else:
+        _, g, src_all = build_graph_ours(wl)
+        O = Oracle()
+        kind, cores = "port", 1
+        step = lambda src: O.bc_eq4(g, sources=src)  # noqa: E731
+    # bounded sample per step: about 3 s of work
+    probe = src_all[: max(1, min(len(src_all), 4 * cores))]
+    t = time.perf_counter()
+    step(probe)
+    per_src = (time.perf_counter() - t) / len(probe)
+    k = int(max(1, min(len(src_all), 3.0 / max(per_src, 1e-9))))
+    if kind == "reference":
+        k = max(cores, k - k % cores) if len(src_all) >= cores else len(src_all)
+    sample = src_all[:k]
+    for _ in range(args.warmup):
+        step(sample)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(sample)
+    dt = time.perf_counter() - t0
+    value = g.m * len(sample) * args.steps / dt / 1e9
+    line = dict(metric=METRIC, value=value, unit="GTEPS", n_gpus=0, steps=args.steps, warmup=args.warmup,
+                ms_per_step=dt / args.steps * 1e3, higher_is_better=True, scaling="none", vs_baseline=None,
+                dtype="f64", data="synthetic", impl="reference",
+                config=dict(workload=wl_name, graph=describe(wl), n=int(g.n), m=int(g.m),
+                            sources_per_step=int(len(sample)),
+                            note="bounded sample of the workload's source list per step"),
+                cpu_baseline=dict(value=value, unit="GTEPS", cores=cores, kind=kind,
+                                  sample=f"{len(sample)} sources per step, bc_parallel strategy="
+                                         f"{BEST_STRATEGY[wl['kind']]} workers={cores}"),
+                e2e=dict(value=value, unit="GTEPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="rmat20", choices=sorted(WORKLOADS))
+    ap.add_argument("--sources", type=int, default=0, help="override the workload's source count")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--slots", type=int, default=0)
+    ap.add_argument("--near", type=int, default=0)
+    args = ap.parse_args()
+    wl = dict(WORKLOADS[args.workload])
+    if args.sources:
+        wl["sources"] = args.sources
+    if args.impl == "reference":
+        return run_reference_arm(args, args.workload, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1701_05975_b200 as W
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    t_build = time.perf_counter()
+    _, g, src_all = build_graph_ours(wl)
+    t_build = time.perf_counter() - t_build
+    gg = W.GpuGraph(g, device=local)
+    gg.set_tuning(args.threads, args.slots, args.near)
+    shard = np.ascontiguousarray(src_all[rank::world])
+    n, m = g.n, g.m
+    stream = torch.cuda.current_stream()
+    d_src = torch.from_numpy(shard.astype(np.int32)).cuda()
+    d_node = torch.zeros(n, dtype=torch.float64, device="cuda")
+    d_depth = torch.zeros(n, dtype=torch.int32, device="cuda")
+
+    def device_step(events=None):
+        d_node.zero_()
+        if events is not None:
+            events[0].record(stream)
+        gg.bc_device(d_src.data_ptr(), len(shard), d_node.data_ptr(), d_depth.data_ptr(),
+                     stream=stream.cuda_stream)
+        if events is not None:
+            events[1].record(stream)
+        if world > 1:
+            dist.all_reduce(d_node)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launch_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                     for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    t_start.record(stream)
+    launches = 0
+    for i in range(args.steps):
+        device_step(launch_events[i])
+        launches += gg.last_run_stats()["launches"]
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    elapsed = t_start.elapsed_time(t_end) / 1e3
+    kernel_s = [a.elapsed_time(b) / 1e3 for a, b in launch_events]
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    total_sources = len(src_all)
+    value = m * total_sources * args.steps / elapsed / 1e9
+    bc_sum = float(d_node.sum().item())
+
+    # ---- e2e through the host-buffer C ABI (wbc_gpu_bc): H2D sources, D2H results
+    opt = W.EngineOptions(sources=shard)
+    host_node = None
+    for _ in range(1):
+        gg.bc(opt)  # warm (allocates host-path scratch)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = gg.bc(opt)
+        host_node = r.node_bc
+        if world > 1:
+            tt = torch.from_numpy(host_node).cuda()
+            dist.all_reduce(tt)
+            host_node = tt.cpu().numpy()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = m * total_sources * args.steps / e2e_s / 1e9
+    h2d = 4 * len(shard) + (8 * n if world > 1 else 0)
+    d2h = 8 * n + 4 * n + 4 + (8 * n if world > 1 else 0)
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        per_launch_bytes = algorithmic_bytes_per_source(n, m) * len(shard)
+        avg_launch = sum(kernel_s) / len(kernel_s)
+        achieved = per_launch_bytes / avg_launch / 1e9
+        tps = load_traffic(args.workload)
+        roofline = dict(bound="hbm", achieved=round(achieved, 1), peak=peak, unit="GB/s",
+                        frac=round(achieved / peak, 4),
+                        traffic=None if tps is None else tps * len(shard),
+                        peak_source=peak_src, kernel="bc_sources_kernel",
+                        bytes_model="72m+88n per source (SURVEY.md 8d)",
+                        launch_ms=round(avg_launch * 1e3, 3))
+        line = dict(metric=METRIC, value=round(value, 3), unit="GTEPS", n_gpus=world, steps=args.steps,
+                    warmup=args.warmup, ms_per_step=round(elapsed / args.steps * 1e3, 3), higher_is_better=True,
+                    scaling="strong", vs_baseline=None, dtype="u32 dist / f64 sigma,delta,BC", data="synthetic",
+                    config=dict(workload=args.workload, graph=describe(wl), n=int(n), m=int(m),
+                                sources_per_step=int(total_sources), parallelism=f"source-partitioned x{world}",
+                                l2="inputs exceed L2 (CSR replica + per-source workspaces >> 126 MB), no flush",
+                                graph_build_s=round(t_build, 2)),
+                    e2e=dict(value=round(e2e_value, 3), unit="GTEPS", h2d_bytes_per_step=int(h2d),
+                             d2h_bytes_per_step=int(d2h), api="wbc_gpu_bc (host buffers)"),
+                    roofline=roofline, clocks=clk, gpu_launches=int(launches),
+                    run_stats=gg.last_run_stats(), bc_checksum=bc_sum)
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                line["cpu_baseline"] = cpu_baseline(args.workload, wl)
+            except Exception as ex:  # reported, never fatal
+                line["cpu_baseline"] = dict(value=None, unit="GTEPS", cores=os.cpu_count(), kind="reference",
+                                            sample=f"failed: {ex}")
+        print(json.dumps(line), flush=True)
+    gg.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

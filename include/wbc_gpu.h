@@ -92,14 +92,30 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
 int wbc_gpu_graph_info(wbc_gpu_graph* g, uint32_t* n, uint32_t* m, uint32_t* max_weight,
                        int* packed_slots, uint32_t* near_width, uint64_t* graph_bytes);
 
-/* Tuning knobs (0 = automatic): threads per CTA (128/256/512), resident
- * source slots (CTAs), near-window width of the pending split. */
+/* Tuning knobs (0 = automatic): threads per CTA (128/256/512/1024),
+ * resident source slots (CTAs), near-window width of the pending split, and
+ * the number of highest-degree vertices whose distances live in shared
+ * memory (-1 = automatic). */
 int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
-                       uint32_t near_width);
+                       uint32_t near_width, int64_t hot_vertices);
+
+/* Named tuning parameter (experiments/benches): "threads", "slots",
+ * "near_width", "hot" (shared-memory distance entries; -1 auto), "l2hot"
+ * (ids whose distance accesses carry an L2 evict-last hint; -1 auto). */
+int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value);
+
+/* Work counters of subsequent runs (off by default; a few atomics per
+ * source): [0] settlement rounds, [1] relaxed slots, [2] near entries
+ * scanned, [3] far entries scanned, [4] far refills, [5] distance
+ * improvements, [6] DAG edges, [7..11] SM clock cycles spent by each CTA in
+ * init / relax / threshold / settle / backward, [12..15] unused.  Summed over
+ * the sources of the last run. */
+int wbc_gpu_set_profiling(wbc_gpu_graph* g, int on);
+int wbc_gpu_profile_counters(wbc_gpu_graph* g, uint64_t* out16);
 
 /* Counters of the last run: [0]=slots used, [1]=threads per CTA,
- * [2]=sources that overflowed the DAG-edge buffer (row-scan fallback),
- * [3]=kernel launches issued by the last wbc_gpu_bc* call. */
+ * [2]=sources that overflowed the DAG-edge buffer (row-scan fallback;
+ * host-buffer runs only), [3]=kernel launches issued by the last call. */
 int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4);
 
 const char* wbc_gpu_last_error(void);

@@ -362,10 +362,28 @@ class GpuGraph:
         return dict(n=n.value, m=m.value, max_weight=mw.value, packed_slots=bool(packed.value),
                     near_width=nw.value, graph_bytes=gb.value)
 
-    def set_tuning(self, threads_per_cta: int = 0, max_slots: int = 0, near_width: int = 0):
-        rc = L.load().wbc_gpu_set_tuning(self._h, threads_per_cta, max_slots, near_width)
+    def set_tuning(self, threads_per_cta: int = 0, max_slots: int = 0, near_width: int = 0,
+                   hot_vertices: int = -1):
+        rc = L.load().wbc_gpu_set_tuning(self._h, threads_per_cta, max_slots, near_width, hot_vertices)
         if rc:
             _raise(rc)
+
+    def set_param(self, name: str, value: int):
+        rc = L.load().wbc_gpu_set_param(self._h, name.encode(), int(value))
+        if rc:
+            _raise(rc)
+
+    def set_profiling(self, on: bool = True):
+        L.load().wbc_gpu_set_profiling(self._h, int(on))
+
+    def profile_counters(self) -> dict:
+        out = np.zeros(16, np.uint64)
+        rc = L.load().wbc_gpu_profile_counters(self._h, _p(out))
+        if rc:
+            _raise(rc)
+        keys = ["rounds", "relaxed_slots", "near_scanned", "far_scanned", "refills", "improvements",
+                "dag_edges", "cyc_init", "cyc_relax", "cyc_threshold", "cyc_settle", "cyc_backward"]
+        return {k: int(v) for k, v in zip(keys, out)}
 
     def last_run_stats(self) -> dict:
         st = np.zeros(4, np.uint64)

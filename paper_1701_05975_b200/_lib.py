@@ -34,7 +34,10 @@ SIGNATURES = [
     ("wbc_gpu_sssp_dump", i32, [vp, u32, vp, vp, vp, C.POINTER(u32)]),
     ("wbc_gpu_graph_info", i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(i32),
                                  C.POINTER(u32), C.POINTER(u64)]),
-    ("wbc_gpu_set_tuning", i32, [vp, i32, i32, u32]),
+    ("wbc_gpu_set_tuning", i32, [vp, i32, i32, u32, i64]),
+    ("wbc_gpu_set_param", i32, [vp, C.c_char_p, i64]),
+    ("wbc_gpu_set_profiling", i32, [vp, i32]),
+    ("wbc_gpu_profile_counters", i32, [vp, vp]),
     ("wbc_gpu_last_run_stats", i32, [vp, vp]),
     ("wbc_gpu_last_error", C.c_char_p, []),
     ("wbc_host_parse_edge_list", i32, [C.c_char_p, C.c_size_t, f64, C.POINTER(vp), C.POINTER(u64)]),

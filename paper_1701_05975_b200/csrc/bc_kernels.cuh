@@ -42,6 +42,44 @@ namespace wbc_dev {
 namespace cg = cooperative_groups;
 
 constexpr uint32_t kInfDist = 0xFFFFFFFFu;
+constexpr int kUnroll = 4;  // independent edge chains per lane in relax
+
+// ---- L2 residency hints.  The CSR slot stream (read once per source, 4 B
+// per slot, far larger than L2) is marked evict-first and skips L1; the
+// distance entries of the highest-degree ids (the ones most neighbour
+// accesses hit) are marked evict-last, so the stream cannot push them out.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* a, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream_u64(const uint2* a, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_cg_hint(const uint32_t* a, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t atom_min_hint(uint32_t* a, uint32_t v, uint64_t pol) {
+  uint32_t r;
+  asm volatile("atom.global.min.u32.L2::cache_hint %0, [%1], %2, %3;" : "=r"(r) : "l"(a), "r"(v), "l"(pol) : "memory");
+  return r;
+}
+
 
 struct GraphView {
   uint32_t n, m;
@@ -80,8 +118,70 @@ struct RunParams {
   uint32_t* depth;         // null or n entries
   uint32_t near_width;     // S: width of the near window
   unsigned int* overflow;  // count of sources that used the row-scan fallback
-  int keep_state;          // debug: zero-copy dump of slot 0 (sigma/delta kept)
+  int keep_state;          // debug: write the shared-memory distances back (dump)
+  const uint32_t* inv;     // original dense id -> device id (degree-descending relabel)
+  uint32_t hot;            // device ids < hot keep their distance in shared memory
+  uint32_t l2hot;          // device ids < l2hot get evict-last L2 hints
+  unsigned long long* prof;  // null or kProfCounters per-run work counters
 };
+
+// Work counters (accumulated per source when RunParams::prof is set).
+enum ProfCounter {
+  kProfRounds = 0,
+  kProfRelaxSlots,
+  kProfNearScanned,
+  kProfFarScanned,
+  kProfRefills,
+  kProfImprovements,
+  kProfDagEdges,
+  kProfCyclesInit,
+  kProfCyclesRelax,
+  kProfCyclesThreshold,
+  kProfCyclesSettle,
+  kProfCyclesBackward,
+  kProfCounters
+};
+
+// Distances: device ids below `hot` live in the CTA's shared memory (the
+// degree-descending relabel puts the vertices that absorb most neighbour
+// accesses there: on R-MAT-20 the top 5% of ids take 69% of them), the rest
+// in the slot's global array.  Values only decrease within a source, so a
+// stale read can only cost an extra atomic, never a wrong result.
+struct DistView {
+  uint32_t* sm;
+  uint32_t* gl;
+  uint32_t hot;     // ids below: shared memory
+  uint32_t l2hot;   // ids below (and >= hot): global with an evict-last hint
+  uint64_t keep;    // evict-last policy
+  __device__ __forceinline__ uint32_t load(uint32_t u) const {
+    if (u < hot) return *(volatile uint32_t*)(sm + u);
+    return u < l2hot ? ld_cg_hint(gl + u, keep) : __ldcg(gl + u);
+  }
+  __device__ __forceinline__ uint32_t fetch_min(uint32_t u, uint32_t v) const {
+    if (u < hot) return atomicMin(sm + u, v);
+    return u < l2hot ? atom_min_hint(gl + u, v, keep) : atomicMin(gl + u, v);
+  }
+  __device__ __forceinline__ void store(uint32_t u, uint32_t v) const {
+    if (u < hot)
+      sm[u] = v;
+    else
+      gl[u] = v;
+  }
+};
+
+template <bool PACKED>
+__device__ __forceinline__ void load_slot(const GraphView& g, uint32_t e, uint32_t& u,
+                                          uint32_t& w, uint64_t pol) {
+  if constexpr (PACKED) {
+    const uint32_t x = ld_stream_u32(g.slots32 + e, pol);
+    u = x >> g.wbits;
+    w = x & g.wmask;
+  } else {
+    const uint2 x = ld_stream_u64(g.slots64 + e, pol);
+    u = x.x;
+    w = x.y;
+  }
+}
 
 template <bool PACKED>
 __device__ __forceinline__ void load_slot(const GraphView& g, uint32_t e, uint32_t& u,
@@ -108,6 +208,56 @@ __device__ __forceinline__ int find_row(const uint32_t* pref, int cnt, uint32_t 
       hi = mid - 1;
   }
   return lo;
+}
+
+// Edge-balanced expansion of a staged chunk without a per-edge search.  The
+// chunk's `total` edges (rows sh.row[j], prefix sh.pref[j], pref[cnt] =
+// total) are cut into one contiguous range per warp; the warp walks its range
+// 32 edges (a "group") at a time.  Every staged row has >= 1 edge (frontier
+// vertices were reached through an edge; an isolated source has total == 0),
+// so a group crosses at most 31 row ends: lane l loads the end of row j0+l,
+// the ends inside the group are OR-reduced into a bit mask, and each lane's
+// row is j0 + popc(mask below its position).  One LDS per lane per 32 edges
+// instead of a log2(T)-step binary search per edge.
+//
+// group_row returns the lane's row for the group starting at e0 and advances
+// j0 to the row holding e0 + 32.
+__device__ __forceinline__ int group_row(const uint32_t* pref, int cnt, uint32_t e0, int& j0) {
+  const int lane = threadIdx.x & 31;
+  const int jl = j0 + 1 + lane;
+  const uint32_t pe = jl <= cnt ? pref[jl] : 0xFFFFFFFFu;
+  const uint32_t q = pe - e0;  // position of a row end inside the group
+  const uint32_t bit = (pe > e0 && q < 32) ? (1u << q) : 0u;
+  const uint32_t mask = __reduce_or_sync(0xffffffffu, bit);
+  const int j = j0 + __popc(mask & ((2u << lane) - 1u));
+  const int j31 = j0 + __popc(mask);
+  j0 = j31 + ((j31 + 1 <= cnt && pref[j31 + 1] <= e0 + 32) ? 1 : 0);
+  return j;
+}
+
+// The warp's contiguous edge range [b, e_end) of a chunk.
+template <int T>
+__device__ __forceinline__ bool warp_range(uint32_t total, uint32_t& b, uint32_t& e_end) {
+  constexpr uint32_t kWarps = T / 32;
+  const uint32_t warp = threadIdx.x >> 5;
+  // round the per-warp share up to whole groups so groups stay aligned
+  const uint32_t per = ((total + kWarps - 1) / kWarps + 31) & ~31u;
+  b = min(total, per * warp);
+  e_end = min(total, b + per);
+  return b < e_end;
+}
+
+// Single-group-per-step expansion (cold paths: the row-scan delta fallback).
+template <int T, class F>
+__device__ __forceinline__ void expand_edges(const uint32_t* pref, int cnt, uint32_t total, F&& f) {
+  uint32_t b, e_end;
+  if (!warp_range<T>(total, b, e_end)) return;
+  int j0 = find_row(pref, cnt, b);
+  for (uint32_t e0 = b; e0 < e_end; e0 += 32) {
+    const int j = group_row(pref, cnt, e0, j0);
+    const uint32_t e = e0 + (threadIdx.x & 31);
+    if (e < e_end) f(e, j);
+  }
 }
 
 // Warp-aggregated append: one shared atomic per converged group.
@@ -143,7 +293,7 @@ struct Shared {
 // the edge total.  Caller must __syncthreads() before reading sh.pref/row.
 template <int T>
 __device__ __forceinline__ uint32_t stage_chunk(const GraphView& g, const uint32_t* order,
-                                                const uint32_t* dist, uint32_t c, int cnt,
+                                                const DistView& dist, uint32_t c, int cnt,
                                                 Shared<T>& sh) {
   using Scan = cub::BlockScan<uint32_t, T, cub::BLOCK_SCAN_WARP_SCANS>;
   const int tid = threadIdx.x;
@@ -153,7 +303,7 @@ __device__ __forceinline__ uint32_t stage_chunk(const GraphView& g, const uint32
     const uint32_t r0 = __ldg(g.offsets + v);
     deg = __ldg(g.offsets + v + 1) - r0;
     sh.v[tid] = v;
-    sh.dv[tid] = __ldcg(dist + v);
+    sh.dv[tid] = dist.load(v);
     sh.row[tid] = r0;
     sh.acc[tid] = 0.0;
   }
@@ -163,13 +313,15 @@ __device__ __forceinline__ uint32_t stage_chunk(const GraphView& g, const uint32
   return total;
 }
 
-template <int T, bool PACKED>
-__global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
+template <int T, bool PACKED, bool PROF>
+__global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1536 / T)) bc_sources_kernel(const RunParams p) {
   __shared__ Shared<T> sh;
+  extern __shared__ uint32_t hot_dist[];
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   const uint64_t off = static_cast<uint64_t>(blockIdx.x) * p.ws.n_stride;
-  uint32_t* const dist = p.ws.dist + off;
+  const DistView dist{hot_dist, p.ws.dist + off, p.hot, p.l2hot, l2_policy_evict_last()};
+  const uint64_t stream_pol = l2_policy_evict_first();
   double* const sigma = p.ws.sigma + off;
   double* const delta = p.ws.delta + off;
   uint32_t* const order = p.ws.order + off;
@@ -181,16 +333,30 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
   const uint32_t dag_cap = static_cast<uint32_t>(p.ws.dag_cap);
   const uint32_t n = g.n;
   const uint32_t S = p.near_width;
+  unsigned long long c_relax = 0, c_near = 0, c_far = 0, c_refill = 0, c_impr = 0;
+  // phase clocks (thread 0, only when profiling)
+  unsigned long long t_last = 0, t_phase[5] = {0, 0, 0, 0, 0};
+  const bool timing = PROF && tid == 0;
+  auto tick = [&](int k) {
+    if (timing) {
+      const unsigned long long t = clock64();
+      t_phase[k] += t - t_last;
+      t_last = t;
+    }
+  };
 
   for (;;) {
     if (tid == 0) sh.src_idx = atomicAdd(p.counter, 1ULL);
     __syncthreads();
     const unsigned long long idx = sh.src_idx;
     if (idx >= p.k) break;
-    const uint32_t s = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(idx);
+    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(idx);
+    const uint32_t s = __ldg(p.inv + s_orig);
+    if (timing) t_last = clock64();
 
     // ---- init_state (engine.cpp:118-142): d = inf, d[s] = 0, level 0 = {s}
-    for (uint32_t i = tid; i < n; i += T) dist[i] = kInfDist;
+    for (uint32_t i = tid; i < p.hot; i += T) hot_dist[i] = kInfDist;
+    for (uint32_t i = p.hot + tid; i < n; i += T) dist.gl[i] = kInfDist;
     if (tid == 0) {
       sh.near_len = 0;
       sh.far_len = 0;
@@ -202,7 +368,7 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
     }
     __syncthreads();
     if (tid == 0) {
-      dist[s] = 0;
+      dist.store(s, 0);
       order[0] = s;
       lev[0] = 0;
       lev[1] = 1;
@@ -210,6 +376,7 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
     }
     __syncthreads();
 
+    tick(0);
     uint32_t fb = 0, fe = 1, nlev = 1;  // frontier = order[fb, fe) = level nlev-1
     uint64_t F = S;                      // near window bound (d < F is near)
     uint32_t kept_min = kInfDist;        // min key of near entries kept by the last settle
@@ -223,32 +390,56 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
         const uint32_t total = stage_chunk<T>(g, order, dist, c, cnt, sh);
         if (tid == 0) sh.pref[cnt] = total;
         __syncthreads();
-        for (uint32_t e = tid; e < total; e += T) {
-          const int j = find_row(sh.pref, cnt, e);
-          const uint32_t slot = sh.row[j] + (e - sh.pref[j]);
-          const uint32_t dv = sh.dv[j];
-          uint32_t u, w;
-          load_slot<PACKED>(g, slot, u, w);
-          const uint32_t du = __ldcg(dist + u);
-          if (dv >= w && du == dv - w) {
-            // u precedes v on a shortest path: u settled in an earlier round,
-            // so sigma[u] is final (see header).
-            atomicAdd(&sh.acc[j], __ldcg(sigma + u));
-            const uint32_t pos = group_append(&sh.dag_len);
-            if (pos < dag_cap)
-              dag[pos] = make_uint2(slot, sh.v[j]);
-            else
-              sh.dag_over = 1;
-          }
-          const uint32_t nd = dv + w;
-          if (nd < du) {
-            const uint32_t old = atomicMin(dist + u, nd);
-            if (nd < old) {
-              if (nd < Fu) {
-                kmin = min(kmin, nd + __ldg(g.minw + u));
-                if (old >= Fu) near_q[group_append(&sh.near_len)] = u;
-              } else if (old == kInfDist) {
-                far_q[group_append(&sh.far_len)] = u;
+        c_relax += total;
+        uint32_t wb, we;
+        if (warp_range<T>(total, wb, we)) {
+          int j0 = find_row(sh.pref, cnt, wb);
+          // kUnroll independent slot -> dist chains per lane: all slot loads,
+          // then all distance loads, then the compare / atomic / append work.
+          for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
+            int jj[kUnroll];
+            uint32_t slot[kUnroll], uu[kUnroll], ww[kUnroll], du[kUnroll];
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k) {
+              const uint32_t eg = e0 + 32 * k;
+              jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0) : 0;
+              const uint32_t e = eg + (tid & 31);
+              slot[k] = e < we ? sh.row[jj[k]] + (e - sh.pref[jj[k]]) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k)
+              if (slot[k] != 0xFFFFFFFFu) load_slot<PACKED>(g, slot[k], uu[k], ww[k], stream_pol);
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k)
+              if (slot[k] != 0xFFFFFFFFu) du[k] = dist.load(uu[k]);
+#pragma unroll
+            for (int k = 0; k < kUnroll; ++k) {
+              if (slot[k] == 0xFFFFFFFFu) continue;
+              const int j = jj[k];
+              const uint32_t u = uu[k], w = ww[k];
+              const uint32_t dv = sh.dv[j];
+              if (dv >= w && du[k] == dv - w) {
+                // u precedes v on a shortest path: u settled in an earlier
+                // round, so sigma[u] is final (see header).
+                atomicAdd(&sh.acc[j], __ldcg(sigma + u));
+                const uint32_t pos = group_append(&sh.dag_len);
+                if (pos < dag_cap)
+                  dag[pos] = make_uint2(slot[k], sh.v[j]);
+                else
+                  sh.dag_over = 1;
+              }
+              const uint32_t nd = dv + w;
+              if (nd < du[k]) {
+                const uint32_t old = dist.fetch_min(u, nd);
+                if (nd < old) {
+                  ++c_impr;
+                  if (nd < Fu) {
+                    kmin = min(kmin, nd + __ldg(g.minw + u));
+                    if (old >= Fu) near_q[group_append(&sh.near_len)] = u;
+                  } else if (old == kInfDist) {
+                    far_q[group_append(&sh.far_len)] = u;
+                  }
+                }
               }
             }
           }
@@ -268,6 +459,7 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
       uint32_t near_len = sh.near_len, far_len = sh.far_len;
       __syncthreads();
       if (tid == 0) sh.key_min = kInfDist;
+      tick(1);
 
       // ---------------- threshold: make the near-only Delta exact
       bool done = (near_len == 0 && far_len == 0);
@@ -287,12 +479,14 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
         }
         __syncthreads();
         uint32_t lkey = kInfDist, lfar = kInfDist;
+        c_far += far_len;
+        ++c_refill;
         for (uint32_t c = 0; c < far_len; c += T) {
           const uint32_t i = c + tid;
           uint32_t u = 0, du = 0;
           if (i < far_len) {
             u = __ldcg(far_q + i);
-            du = __ldcg(dist + u);
+            du = dist.load(u);
           }
           __syncthreads();
           if (i < far_len && du >= Fo) {  // du < Fo: already near or settled
@@ -321,6 +515,7 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
         }
         done = (near_len == 0 && far_len == 0);
       }
+      tick(2);
       if (done) break;
 
       // ---------------- settle: d < Delta joins level nlev (in-place compaction)
@@ -328,12 +523,13 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
       __syncthreads();
       const uint32_t before = sh.order_len;
       uint32_t lkept = kInfDist;
+      c_near += near_len;
       for (uint32_t c = 0; c < near_len; c += T) {
         const uint32_t i = c + tid;
         uint32_t u = 0, du = 0;
         if (i < near_len) {
           u = __ldcg(near_q + i);
-          du = __ldcg(dist + u);
+          du = dist.load(u);
         }
         __syncthreads();
         if (i < near_len) {
@@ -358,6 +554,7 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
       fb = before;
       fe = after;
       ++nlev;
+      tick(3);
       // (the next relax's first __syncthreads orders these smem writes)
     }
 
@@ -397,19 +594,18 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
           const uint32_t total = stage_chunk<T>(g, order, dist, c, cnt, sh);
           if (tid == 0) sh.pref[cnt] = total;
           __syncthreads();
-          for (uint32_t e = tid; e < total; e += T) {
-            const int j = find_row(sh.pref, cnt, e);
+          expand_edges<T>(sh.pref, cnt, total, [&](uint32_t e, int j) {
             const uint32_t slot = sh.row[j] + (e - sh.pref[j]);
             uint32_t x, w;
             load_slot<PACKED>(g, slot, x, w);
-            const uint32_t dx = __ldcg(dist + x);
+            const uint32_t dx = dist.load(x);
             if (dx != kInfDist && dx == sh.dv[j] + w) {
               const uint32_t wv = sh.v[j];
               const double c2 = __ldcg(sigma + wv) / __ldcg(sigma + x) * (1.0 + __ldcg(delta + x));
               atomicAdd(&sh.acc[j], c2);
               if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + slot), c2);
             }
-          }
+          });
           __syncthreads();
           if (tid < cnt) {
             const uint32_t wv = sh.v[tid];
@@ -420,7 +616,29 @@ __global__ void __launch_bounds__(T) bc_sources_kernel(const RunParams p) {
         }
       }
     }
-    if (tid == 0 && p.depth) p.depth[s] = nlev;
+    __syncthreads();
+    tick(4);
+    if (tid == 0 && p.depth) p.depth[s_orig] = nlev;
+    if (p.keep_state)
+      for (uint32_t i = tid; i < p.hot; i += T) dist.gl[i] = hot_dist[i];
+    if (PROF && tid == 0) {
+      atomicAdd(p.prof + kProfRounds, nlev);
+      atomicAdd(p.prof + kProfDagEdges, sh.dag_len);
+      atomicAdd(p.prof + kProfRelaxSlots, c_relax);
+      atomicAdd(p.prof + kProfNearScanned, c_near);
+      atomicAdd(p.prof + kProfFarScanned, c_far);
+      atomicAdd(p.prof + kProfRefills, c_refill);
+      for (int k = 0; k < 5; ++k) {
+        atomicAdd(p.prof + kProfCyclesInit + k, t_phase[k]);
+        t_phase[k] = 0;
+      }
+      c_relax = c_near = c_far = c_refill = 0;
+    }
+    if (PROF) {
+      c_impr = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c_impr));
+      if ((tid & 31) == 0) atomicAdd(p.prof + kProfImprovements, c_impr);
+      c_impr = 0;
+    }
     __syncthreads();
   }
 }
@@ -429,6 +647,13 @@ __global__ void scale_kernel(double* x, uint64_t len, double f) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     x[i] *= f;
+}
+
+// out[perm[i]] += in[i]: device-id partial BC back to original dense ids.
+__global__ void scatter_add_kernel(double* out, const double* in, const uint32_t* perm, uint64_t len) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[perm[i]] += in[i];
 }
 
 __global__ void fill_u32_kernel(uint32_t* x, uint64_t len, uint32_t v) {

@@ -81,7 +81,7 @@ GpuBcEngine::GpuBcEngine(const CsrGraph& g, const GpuOptions& gpu)
                                       &impl_->h);
   if (rc) throw_status(rc);
   if (gpu.threads_per_cta || gpu.max_slots)
-    wbc_gpu_set_tuning(impl_->h, gpu.threads_per_cta, gpu.max_slots, 0);
+    wbc_gpu_set_tuning(impl_->h, gpu.threads_per_cta, gpu.max_slots, 0, -1);
 }
 
 GpuBcEngine::~GpuBcEngine() = default;

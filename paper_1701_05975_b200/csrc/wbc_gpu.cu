@@ -5,6 +5,11 @@
 // launches the persistent per-source kernel (bc_kernels.cuh) on the caller's
 // stream.  No CPU fallback exists: without a device every entry point fails
 // with WBC_E_CUDA / WBC_E_NOT_BUILT.
+//
+// Device layout: vertices are relabelled by degree, highest
+// first (ties by id), each row's slots sorted by relabelled neighbour, and a
+// slot is one u32 (neighbour << wbits | weight) when it fits, else a uint2.
+// Results are mapped back to the caller's dense ids on the device.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -12,7 +17,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "bc_kernels.cuh"
@@ -48,6 +55,24 @@ uint32_t bits_for(uint64_t x) {  // bits needed to store values 0..x
   return b;
 }
 
+uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+template <class F>
+void parallel_for(uint64_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  if (n < 65536 || hw == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> ts;
+  const uint64_t chunk = (n + hw - 1) / hw;
+  for (unsigned t = 0; t < hw; ++t) {
+    const uint64_t b = t * chunk, e = std::min(n, b + chunk);
+    if (b < e) ts.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& t : ts) t.join();
+}
+
 }  // namespace
 
 namespace wbc_host {
@@ -63,20 +88,27 @@ struct wbc_gpu_graph {
   uint32_t wbits = 0;
   uint32_t near_width = 1;
   int sm_count = 0;
-  // device CSR replica
+  int smem_per_sm = 0;
+  int smem_optin = 0;
+  double hot_coverage_25k = 0;  // share of neighbour accesses landing on the top 25K ids
+  // device CSR replica (relabelled ids)
   uint32_t* d_offsets = nullptr;
   uint32_t* d_slots32 = nullptr;
   uint2* d_slots64 = nullptr;
   uint32_t* d_minw = nullptr;
   uint32_t* d_edge_id = nullptr;
+  uint32_t* d_perm = nullptr;  // device id -> caller id
+  uint32_t* d_inv = nullptr;   // caller id -> device id
+  std::vector<uint32_t> perm;  // host copy
   uint64_t graph_bytes = 0;
   // workspace
   int ws_slots = 0;
-  int ws_threads = 0;
   void* d_ws = nullptr;
   wbc_dev::Workspace ws{};
   unsigned long long* d_counter = nullptr;
   unsigned int* d_overflow = nullptr;
+  unsigned long long* d_prof = nullptr;
+  double* d_node_dev = nullptr;  // device-id partial BC of the current run
   // scratch for host-buffer runs
   double* d_node = nullptr;
   double* d_edge = nullptr;
@@ -86,22 +118,19 @@ struct wbc_gpu_graph {
   // tuning
   int tune_threads = 0;
   int tune_slots = 0;
+  int64_t tune_hot = -1;
+  int64_t tune_l2hot = -1;
+  bool profiling = false;
   uint64_t stats[4] = {0, 0, 0, 0};
+  uint64_t prof_host[wbc_dev::kProfCounters] = {};
 
   ~wbc_gpu_graph() {
     cudaSetDevice(device);
-    cudaFree(d_offsets);
-    cudaFree(d_slots32);
-    cudaFree(d_slots64);
-    cudaFree(d_minw);
-    cudaFree(d_edge_id);
-    cudaFree(d_ws);
-    cudaFree(d_counter);
-    cudaFree(d_overflow);
-    cudaFree(d_node);
-    cudaFree(d_edge);
-    cudaFree(d_depth);
-    cudaFree(d_sources);
+    for (void* p : {(void*)d_offsets, (void*)d_slots32, (void*)d_slots64, (void*)d_minw,
+                    (void*)d_edge_id, (void*)d_perm, (void*)d_inv, d_ws, (void*)d_counter,
+                    (void*)d_overflow, (void*)d_prof, (void*)d_node_dev, (void*)d_node,
+                    (void*)d_edge, (void*)d_depth, (void*)d_sources})
+      cudaFree(p);
   }
 };
 
@@ -109,54 +138,100 @@ namespace {
 
 using KernelFn = void (*)(const wbc_dev::RunParams);
 
-KernelFn pick_kernel(int threads, bool packed) {
+template <bool PACKED, bool PROF>
+KernelFn pick_kernel_t(int threads) {
   using namespace wbc_dev;
-  if (packed) {
-    if (threads <= 128) return bc_sources_kernel<128, true>;
-    if (threads <= 256) return bc_sources_kernel<256, true>;
-    return bc_sources_kernel<512, true>;
+  if (threads <= 128) return bc_sources_kernel<128, PACKED, PROF>;
+  if (threads <= 256) return bc_sources_kernel<256, PACKED, PROF>;
+  if (threads <= 512) return bc_sources_kernel<512, PACKED, PROF>;
+  return bc_sources_kernel<1024, PACKED, PROF>;
+}
+
+KernelFn pick_kernel(int threads, bool packed, bool prof = false) {
+  if (packed) return prof ? pick_kernel_t<true, true>(threads) : pick_kernel_t<true, false>(threads);
+  return prof ? pick_kernel_t<false, true>(threads) : pick_kernel_t<false, false>(threads);
+}
+
+struct LaunchShape {
+  int threads = 128;
+  uint32_t hot = 0;        // vertices with shared-memory distances
+  uint32_t l2hot = 0;      // vertices whose distance accesses carry an evict-last hint
+  size_t dyn_smem = 0;     // bytes
+};
+
+// Launch shape policy:
+//  * small graphs (n*4 <= 24 KB): every distance in shared memory, 128-thread
+//    CTAs, many sources in flight;
+//  * skewed graphs (the top 25K ids take >= 40% of neighbour accesses: R-MAT,
+//    BA): 512-thread CTAs for the large frontiers;
+//  * flat graphs (grid, sparse ER): 128-thread CTAs, many sources in flight;
+//    the per-round latency dominates.
+// Unless tuned, the shared-memory distance cache gets exactly the shared
+// memory left over at the register-limited occupancy, so it never costs
+// resident sources.
+LaunchShape pick_shape(const wbc_gpu_graph* g) {
+  LaunchShape s;
+  const uint64_t n = g->n;
+  const bool tiny = n * 4 <= 24 * 1024;
+  if (g->tune_threads)
+    s.threads = g->tune_threads <= 128 ? 128 : g->tune_threads <= 256 ? 256 : g->tune_threads <= 512 ? 512 : 1024;
+  else if (!tiny && g->hot_coverage_25k >= 0.4)
+    s.threads = 1024;
+  else
+    s.threads = 128;
+  const void* fn = reinterpret_cast<const void*>(pick_kernel(s.threads, g->packed));
+  cudaFuncAttributes attr{};
+  cudaFuncGetAttributes(&attr, fn);
+  const uint64_t cap = (static_cast<uint64_t>(g->smem_optin) - attr.sharedSizeBytes) / 4;
+  uint64_t hot;
+  if (g->tune_hot >= 0) {
+    hot = static_cast<uint64_t>(g->tune_hot);
+  } else if (tiny) {
+    hot = n;
+  } else if (s.threads >= 1024) {
+    hot = 0;  // measured: the L2-hinted global path beats a shared-memory cache here
+  } else {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, s.threads, 0);
+    per_sm = std::max(1, per_sm);
+    const int64_t per_cta = static_cast<int64_t>(g->smem_per_sm) / per_sm - 1024 -
+                            static_cast<int64_t>(attr.sharedSizeBytes);
+    hot = per_cta > 0 ? static_cast<uint64_t>(per_cta) / 4 / 256 * 256 : 0;
   }
-  if (threads <= 128) return bc_sources_kernel<128, false>;
-  if (threads <= 256) return bc_sources_kernel<256, false>;
-  return bc_sources_kernel<512, false>;
+  hot = std::min<uint64_t>(std::min<uint64_t>(hot, n), cap);
+  s.hot = static_cast<uint32_t>(hot);
+  s.dyn_smem = hot * 4;
+  return s;
 }
 
-int auto_threads(const wbc_gpu_graph* g) {
-  if (g->tune_threads) return g->tune_threads <= 128 ? 128 : (g->tune_threads <= 256 ? 256 : 512);
-  // Small frontiers (low average degree, small n) waste wide CTAs.
-  const double avg_deg = g->n ? 2.0 * g->m / g->n : 0.0;
-  if (g->n < 16384 || avg_deg < 6.0) return 128;
-  return 256;
-}
-
-uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
-
-// Ensure a workspace for `want` slots with `threads` per CTA exists.
-int ensure_workspace(wbc_gpu_graph* g, int want, int threads) {
+// Ensure a workspace for `want` slots exists (shape-dependent occupancy).
+int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   const uint64_t ns = round_up(uint64_t{g->n} + 2, 64);
   const uint64_t dag_cap = round_up(uint64_t{g->n} + uint64_t{g->n} / 2 + 1024, 64);
   const uint64_t per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + dag_cap * 8;
-  // occupancy cap
+  const KernelFn fn = pick_kernel(shape.threads, g->packed);
+  for (const bool prof : {false, true})
+    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(shape.dyn_smem)));
   int per_sm = 0;
   WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, reinterpret_cast<const void*>(pick_kernel(threads, g->packed)), threads, 0));
-  int slots = std::max(1, per_sm) * g->sm_count;
+      &per_sm, reinterpret_cast<const void*>(fn), shape.threads, shape.dyn_smem));
+  if (per_sm < 1) return set_error(WBC_E_CUDA, "kernel does not fit on an SM with this launch shape");
+  int slots = per_sm * g->sm_count;
   if (g->tune_slots) slots = std::min(slots, g->tune_slots);
-  slots = std::min(slots, want);
-  // memory cap: keep 4 GiB + 10% headroom
+  slots = std::max(1, std::min(slots, want));
   size_t free_b = 0, total_b = 0;
   WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   uint64_t avail = free_b + (g->d_ws ? uint64_t(g->ws_slots) * per_slot : 0);
-  const uint64_t reserve = (4ULL << 30) + total_b / 10;
+  const uint64_t reserve = (4ULL << 30) + total_b / 10;  // 4 GiB + 10% headroom
   avail = avail > reserve ? avail - reserve : 0;
   slots = static_cast<int>(std::min<uint64_t>(slots, std::max<uint64_t>(1, avail / per_slot)));
-  if (g->d_ws && g->ws_slots >= slots && g->ws_threads == threads) return WBC_OK;
-  if (g->d_ws && g->ws_slots >= slots) {
-    g->ws_threads = threads;
-    return WBC_OK;
-  }
+  *slots_out = slots;
+  if (g->d_ws && g->ws_slots >= slots) return WBC_OK;
   cudaFree(g->d_ws);
   g->d_ws = nullptr;
+  g->ws_slots = 0;
   void* base = nullptr;
   const cudaError_t err = cudaMalloc(&base, per_slot * slots);
   if (err != cudaSuccess)
@@ -164,7 +239,6 @@ int ensure_workspace(wbc_gpu_graph* g, int want, int threads) {
                                       " bytes failed: " + cudaGetErrorString(err));
   g->d_ws = base;
   g->ws_slots = slots;
-  g->ws_threads = threads;
   char* p = static_cast<char*>(base);
   auto carve = [&](uint64_t bytes) {
     char* q = p;
@@ -185,17 +259,21 @@ int ensure_workspace(wbc_gpu_graph* g, int want, int threads) {
   return WBC_OK;
 }
 
-// Enqueue one run: d_sources may be null (all vertices).  Accumulates.
+int launch_grid(uint64_t len) { return static_cast<int>(std::min<uint64_t>((len + 255) / 256, 4096)); }
+
+// Enqueue one run: d_sources may be null (all vertices).  Accumulates node BC
+// (caller ids) into d_node, edge BC into d_edge; writes depth of run sources.
 int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edge_bc,
                double* d_node, double* d_edge, uint32_t* d_depth, cudaStream_t stream,
-               bool single_slot) {
+               bool single_slot, bool keep_state) {
   g->stats[3] = 0;
   if (k == 0 || g->n == 0) return WBC_OK;
-  const int threads = auto_threads(g);
+  const LaunchShape shape = pick_shape(g);
   const int want = single_slot ? 1 : static_cast<int>(std::min<uint64_t>(k, 1u << 30));
-  int rc = ensure_workspace(g, want, threads);
+  int slots = 0;
+  int rc = ensure_workspace(g, want, shape, &slots);
   if (rc) return rc;
-  const int slots = single_slot ? 1 : static_cast<int>(std::min<uint64_t>(g->ws_slots, k));
+  if (single_slot) slots = 1;
   wbc_dev::RunParams p{};
   p.g.n = g->n;
   p.g.m = g->m;
@@ -210,25 +288,38 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   p.sources = d_sources;
   p.k = k;
   p.counter = g->d_counter;
-  p.node_bc = d_node;
+  p.node_bc = g->d_node_dev;
   p.edge_bc = edge_bc ? d_edge : nullptr;
   p.depth = d_depth;
   p.near_width = g->near_width;
   p.overflow = g->d_overflow;
+  p.keep_state = keep_state ? 1 : 0;
+  p.inv = g->d_inv;
+  p.hot = shape.hot;
+  // evict-last budget: ~48 MB of the 126 MB L2 for the hottest distances of
+  // all resident sources together.
+  p.l2hot = g->tune_l2hot >= 0
+                ? static_cast<uint32_t>(std::min<int64_t>(g->tune_l2hot, g->n))
+                : static_cast<uint32_t>(std::min<uint64_t>(g->n, (48ULL << 20) / 4 / std::max(1, slots)));
+  p.prof = g->profiling ? g->d_prof : nullptr;
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter, 0, sizeof(unsigned long long), stream));
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_overflow, 0, sizeof(unsigned int), stream));
-  pick_kernel(threads, g->packed)<<<slots, threads, 0, stream>>>(p);
+  WBC_CUDA_TRY(cudaMemsetAsync(g->d_node_dev, 0, uint64_t{g->n} * 8, stream));
+  if (g->profiling)
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_prof, 0, sizeof(unsigned long long) * wbc_dev::kProfCounters, stream));
+  pick_kernel(shape.threads, g->packed, g->profiling)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p);
+  WBC_CUDA_TRY(cudaGetLastError());
+  wbc_dev::scatter_add_kernel<<<launch_grid(g->n), 256, 0, stream>>>(d_node, g->d_node_dev, g->d_perm, g->n);
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
-  g->stats[1] = threads;
-  g->stats[3] = 1;
+  g->stats[1] = shape.threads;
+  g->stats[3] = 2;
   return WBC_OK;
 }
 
 int scale_async(double* x, uint64_t len, double f, cudaStream_t stream) {
   if (!len) return WBC_OK;
-  const int blocks = static_cast<int>(std::min<uint64_t>((len + 255) / 256, 4096));
-  wbc_dev::scale_kernel<<<blocks, 256, 0, stream>>>(x, len, f);
+  wbc_dev::scale_kernel<<<launch_grid(len), 256, 0, stream>>>(x, len, f);
   WBC_CUDA_TRY(cudaGetLastError());
   return WBC_OK;
 }
@@ -253,6 +344,7 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
     return set_error(WBC_E_INVALID, "adjacency / weights are required");
   if (n > 0 && (offsets[0] != 0 || offsets[n] != slots))
     return set_error(WBC_E_INVALID, "offsets must start at 0 and end at 2m");
+  if (n == 0 && slots != 0) return set_error(WBC_E_INVALID, "edges without vertices");
   for (uint32_t v = 0; v < n; ++v)
     if (offsets[v + 1] < offsets[v]) return set_error(WBC_E_INVALID, "offsets not monotone");
   uint64_t maxw = 0;
@@ -270,11 +362,9 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
 
   auto g = new wbc_gpu_graph();
   int dev = device;
-  if (dev < 0) {
-    if (cudaGetDevice(&dev) != cudaSuccess) {
-      delete g;
-      return set_error(WBC_E_NOT_BUILT, "no CUDA device available");
-    }
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+    delete g;
+    return set_error(WBC_E_NOT_BUILT, "no CUDA device available");
   }
   g->device = dev;
   cudaError_t err = cudaSetDevice(dev);
@@ -285,6 +375,8 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
   int major = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&g->sm_count, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&g->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&g->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (major < 10) {
     delete g;
     return set_error(WBC_E_NOT_BUILT, "device is not sm_100 class (built for sm_100a only)");
@@ -296,35 +388,78 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
   const uint32_t nbits = bits_for(n ? n - 1 : 0);
   g->packed = (g->wbits + nbits) <= 32;
 
-  // Host-side packing of the device CSR replica.
+  // ---- degree-descending relabel (ties by id) ---------------------------
+  std::vector<uint32_t>& perm = g->perm;
+  perm.resize(n);
+  std::iota(perm.begin(), perm.end(), 0u);
+  std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+    return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
+  });
+  std::vector<uint32_t> inv(n);
+  for (uint32_t i = 0; i < n; ++i) inv[perm[i]] = i;
+  std::vector<uint32_t> noff(uint64_t{n} + 1, 0);
+  for (uint32_t i = 0; i < n; ++i) noff[i + 1] = noff[i] + (offsets[perm[i] + 1] - offsets[perm[i]]);
+  if (slots) {
+    uint64_t top = 0;
+    for (uint32_t i = 0; i < std::min<uint32_t>(n, 25 * 1024); ++i) top += noff[i + 1] - noff[i];
+    g->hot_coverage_25k = static_cast<double>(top) / static_cast<double>(slots);
+  }
+  std::vector<uint32_t> slot32(g->packed ? slots : 0);
+  std::vector<uint2> slot64(g->packed ? 0 : slots);
+  std::vector<uint32_t> eid(edge_id ? slots : 0);
   std::vector<uint32_t> minw(n);
   double sum_minw = 0;
   uint64_t cnt_minw = 0;
-  for (uint32_t v = 0; v < n; ++v) {
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t v = perm[i];
     const double x = min_incident_weight[v];
     if (std::isinf(x) || offsets[v + 1] == offsets[v]) {
-      minw[v] = wbc_dev::kInfDist;
+      minw[i] = wbc_dev::kInfDist;
     } else {
-      minw[v] = static_cast<uint32_t>(x);
+      minw[i] = static_cast<uint32_t>(x);
       sum_minw += x;
       ++cnt_minw;
     }
   }
+  const uint32_t wbits = g->wbits;
+  const bool packed = g->packed;
+  parallel_for(n, [&](uint64_t b, uint64_t e) {
+    std::vector<std::pair<uint32_t, uint32_t>> row;  // (new neighbour, old slot)
+    for (uint64_t i = b; i < e; ++i) {
+      const uint32_t v = perm[i];
+      row.clear();
+      for (uint32_t s = offsets[v]; s < offsets[v + 1]; ++s) row.emplace_back(inv[adjacency[s]], s);
+      std::sort(row.begin(), row.end());
+      uint32_t o = noff[i];
+      for (const auto& [u, s] : row) {
+        const uint32_t w = static_cast<uint32_t>(weights[s]);
+        if (packed)
+          slot32[o] = (u << wbits) | w;
+        else
+          slot64[o] = make_uint2(u, w);
+        if (edge_id) eid[o] = edge_id[s];
+        ++o;
+      }
+    }
+  });
   // Near-window width: about half the mean minimum incident weight balances
-  // near rescans against far refills (SURVEY-style sizing in DESIGN.md).
+  // near rescans against far refills.
   g->near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 2.0 + 0.5))
                            : 1;
 
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
   if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);
+  if (err == cudaSuccess) g->d_perm = dev_alloc<uint32_t>(n, err);
+  if (err == cudaSuccess) g->d_inv = dev_alloc<uint32_t>(n, err);
+  if (err == cudaSuccess) g->d_node_dev = dev_alloc<double>(n, err);
   if (err == cudaSuccess) g->d_counter = dev_alloc<unsigned long long>(1, err);
   if (err == cudaSuccess) g->d_overflow = dev_alloc<unsigned int>(1, err);
+  if (err == cudaSuccess) g->d_prof = dev_alloc<unsigned long long>(wbc_dev::kProfCounters, err);
   if (err == cudaSuccess) {
-    if (g->packed) {
+    if (packed)
       g->d_slots32 = dev_alloc<uint32_t>(slots, err);
-    } else {
+    else
       g->d_slots64 = dev_alloc<uint2>(slots, err);
-    }
   }
   if (err == cudaSuccess && edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
   if (err != cudaSuccess) {
@@ -332,29 +467,24 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
     return set_error(WBC_E_NOMEM, std::string("graph upload: ") + cudaGetErrorString(err));
   }
   if (n) {
-    err = cudaMemcpy(g->d_offsets, offsets, (uint64_t{n} + 1) * 4, cudaMemcpyHostToDevice);
+    err = cudaMemcpy(g->d_offsets, noff.data(), (uint64_t{n} + 1) * 4, cudaMemcpyHostToDevice);
     if (err == cudaSuccess) err = cudaMemcpy(g->d_minw, minw.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_perm, perm.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_inv, inv.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
   }
   if (err == cudaSuccess && slots) {
-    if (g->packed) {
-      std::vector<uint32_t> packed(slots);
-      for (uint64_t e = 0; e < slots; ++e)
-        packed[e] = (adjacency[e] << g->wbits) | static_cast<uint32_t>(weights[e]);
-      err = cudaMemcpy(g->d_slots32, packed.data(), slots * 4, cudaMemcpyHostToDevice);
-    } else {
-      std::vector<uint2> wide(slots);
-      for (uint64_t e = 0; e < slots; ++e)
-        wide[e] = make_uint2(adjacency[e], static_cast<uint32_t>(weights[e]));
-      err = cudaMemcpy(g->d_slots64, wide.data(), slots * 8, cudaMemcpyHostToDevice);
-    }
+    if (packed)
+      err = cudaMemcpy(g->d_slots32, slot32.data(), slots * 4, cudaMemcpyHostToDevice);
+    else
+      err = cudaMemcpy(g->d_slots64, slot64.data(), slots * 8, cudaMemcpyHostToDevice);
     if (err == cudaSuccess && edge_id)
-      err = cudaMemcpy(g->d_edge_id, edge_id, slots * 4, cudaMemcpyHostToDevice);
+      err = cudaMemcpy(g->d_edge_id, eid.data(), slots * 4, cudaMemcpyHostToDevice);
   }
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_CUDA, std::string("graph upload: ") + cudaGetErrorString(err));
   }
-  g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 4 + slots * (g->packed ? 4 : 8) +
+  g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 12 + slots * (packed ? 4 : 8) +
                    (edge_id ? slots * 4 : 0);
   *out = g;
   return WBC_OK;
@@ -374,19 +504,44 @@ int wbc_gpu_graph_info(wbc_gpu_graph* g, uint32_t* n, uint32_t* m, uint32_t* max
   return WBC_OK;
 }
 
-int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uint32_t near_width) {
+int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uint32_t near_width,
+                       int64_t hot_vertices) {
   if (!g) return set_error(WBC_E_INVALID, "null graph");
   if (threads_per_cta < 0 || max_slots < 0) return set_error(WBC_E_INVALID, "negative tuning value");
   g->tune_threads = threads_per_cta;
   g->tune_slots = max_slots;
+  g->tune_hot = hot_vertices;
   if (near_width) g->near_width = near_width;
-  if (g->d_ws && max_slots && g->ws_slots > max_slots) {
-    // shrink lazily: next run re-carves with fewer slots
-    cudaSetDevice(g->device);
-    cudaFree(g->d_ws);
-    g->d_ws = nullptr;
-    g->ws_slots = 0;
-  }
+  return WBC_OK;
+}
+
+int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
+  if (!g || !name) return set_error(WBC_E_INVALID, "null argument");
+  const std::string k = name;
+  if (k == "threads") g->tune_threads = static_cast<int>(value);
+  else if (k == "slots") g->tune_slots = static_cast<int>(value);
+  else if (k == "near_width") g->near_width = value > 0 ? static_cast<uint32_t>(value) : g->near_width;
+  else if (k == "hot") g->tune_hot = value;
+  else if (k == "l2hot") g->tune_l2hot = value;
+  else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
+  return WBC_OK;
+}
+
+int wbc_gpu_set_profiling(wbc_gpu_graph* g, int on) {
+  if (!g) return set_error(WBC_E_INVALID, "null graph");
+  g->profiling = on != 0;
+  return WBC_OK;
+}
+
+int wbc_gpu_profile_counters(wbc_gpu_graph* g, uint64_t* out16) {
+  if (!g || !out16) return set_error(WBC_E_INVALID, "null argument");
+  WBC_CUDA_TRY(cudaSetDevice(g->device));
+  WBC_CUDA_TRY(cudaDeviceSynchronize());
+  uint64_t tmp[16] = {};
+  static_assert(wbc_dev::kProfCounters <= 16, "counter block");
+  WBC_CUDA_TRY(cudaMemcpy(tmp, g->d_prof, sizeof(unsigned long long) * wbc_dev::kProfCounters,
+                          cudaMemcpyDeviceToHost));
+  std::memcpy(out16, tmp, sizeof tmp);
   return WBC_OK;
 }
 
@@ -408,7 +563,8 @@ int wbc_gpu_bc_device(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, u
   WBC_CUDA_TRY(cudaSetDevice(g->device));
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t kk = d_sources ? k : g->n;
-  int rc = launch_run(g, d_sources, kk, edge, d_node_bc, d_edge_bc, d_depth_per_source, st, false);
+  int rc = launch_run(g, d_sources, kk, edge, d_node_bc, d_edge_bc, d_depth_per_source, st, false,
+                      false);
   if (rc) return rc;
   if (flags & WBC_HALVED) {
     if ((rc = scale_async(d_node_bc, g->n, 0.5, st))) return rc;
@@ -455,7 +611,7 @@ int wbc_gpu_bc(wbc_gpu_graph* g, const uint32_t* sources, uint64_t k, uint32_t f
   }
   if (edge && g->m) WBC_CUDA_TRY(cudaMemsetAsync(g->d_edge, 0, uint64_t{g->m} * 8, st));
   int rc = launch_run(g, sources ? g->d_sources : nullptr, kk, edge, g->d_node, g->d_edge,
-                      g->d_depth, st, false);
+                      g->d_depth, st, false, false);
   if (rc) return rc;
   if (flags & WBC_HALVED) {  // engine.cpp:451-454
     if ((rc = scale_async(g->d_node, g->n, 0.5, st))) return rc;
@@ -483,35 +639,50 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
   if (!g) return set_error(WBC_E_INVALID, "null graph");
   if (source >= g->n) return set_error(WBC_E_INVALID, "init_state: source out of range");
   WBC_CUDA_TRY(cudaSetDevice(g->device));
-  const int threads = auto_threads(g);
-  int rc = ensure_workspace(g, 1, threads);
+  const uint64_t n = g->n;
+  int slots = 0;
+  int rc = ensure_workspace(g, 1, pick_shape(g), &slots);
   if (rc) return rc;
   cudaError_t err = cudaSuccess;
-  double* d_scratch = dev_alloc<double>(g->n, err);
-  uint32_t* d_src = dev_alloc<uint32_t>(1, err);
-  uint32_t* d_dep = dev_alloc<uint32_t>(g->n, err);
-  if (err != cudaSuccess) return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
-  const uint64_t n = g->n;
-  WBC_CUDA_TRY(cudaMemcpy(d_src, &source, 4, cudaMemcpyHostToDevice));
-  WBC_CUDA_TRY(cudaMemset(d_scratch, 0, n * 8));
-  WBC_CUDA_TRY(cudaMemset(d_dep, 0, n * 4));
-  WBC_CUDA_TRY(cudaMemset(g->ws.sigma, 0, n * 8));  // slot 0: unreached stay 0
-  WBC_CUDA_TRY(cudaMemset(g->ws.delta, 0, n * 8));
-  rc = launch_run(g, d_src, 1, false, d_scratch, nullptr, d_dep, 0, true);
-  if (rc) return rc;
-  WBC_CUDA_TRY(cudaDeviceSynchronize());
+  double* d_scratch = dev_alloc<double>(n, err);
+  uint32_t* d_src = err == cudaSuccess ? dev_alloc<uint32_t>(1, err) : nullptr;
+  uint32_t* d_dep = err == cudaSuccess ? dev_alloc<uint32_t>(n, err) : nullptr;
+  if (err != cudaSuccess) {
+    cudaFree(d_scratch);
+    cudaFree(d_src);
+    return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
+  }
   std::vector<uint32_t> du(n);
-  WBC_CUDA_TRY(cudaMemcpy(du.data(), g->ws.dist, n * 4, cudaMemcpyDeviceToHost));
-  if (dist)
-    for (uint64_t i = 0; i < n; ++i)
-      dist[i] = du[i] == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(du[i]);
-  if (sigma) WBC_CUDA_TRY(cudaMemcpy(sigma, g->ws.sigma, n * 8, cudaMemcpyDeviceToHost));
-  if (delta) WBC_CUDA_TRY(cudaMemcpy(delta, g->ws.delta, n * 8, cudaMemcpyDeviceToHost));
-  if (depth) WBC_CUDA_TRY(cudaMemcpy(depth, d_dep + source, 4, cudaMemcpyDeviceToHost));
+  std::vector<double> tmp(n);
+  auto body = [&]() -> int {
+    WBC_CUDA_TRY(cudaMemcpy(d_src, &source, 4, cudaMemcpyHostToDevice));
+    WBC_CUDA_TRY(cudaMemset(d_scratch, 0, n * 8));
+    WBC_CUDA_TRY(cudaMemset(d_dep, 0, n * 4));
+    WBC_CUDA_TRY(cudaMemset(g->ws.sigma, 0, n * 8));  // slot 0: unreached stay 0
+    WBC_CUDA_TRY(cudaMemset(g->ws.delta, 0, n * 8));
+    int r = launch_run(g, d_src, 1, false, d_scratch, nullptr, d_dep, 0, true, true);
+    if (r) return r;
+    WBC_CUDA_TRY(cudaDeviceSynchronize());
+    WBC_CUDA_TRY(cudaMemcpy(du.data(), g->ws.dist, n * 4, cudaMemcpyDeviceToHost));
+    if (dist)
+      for (uint64_t i = 0; i < n; ++i)
+        dist[g->perm[i]] = du[i] == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(du[i]);
+    if (sigma) {
+      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), g->ws.sigma, n * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < n; ++i) sigma[g->perm[i]] = tmp[i];
+    }
+    if (delta) {
+      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), g->ws.delta, n * 8, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < n; ++i) delta[g->perm[i]] = tmp[i];
+    }
+    if (depth) WBC_CUDA_TRY(cudaMemcpy(depth, d_dep + source, 4, cudaMemcpyDeviceToHost));
+    return WBC_OK;
+  };
+  rc = body();
   cudaFree(d_scratch);
   cudaFree(d_src);
   cudaFree(d_dep);
-  return WBC_OK;
+  return rc;
 }
 
 }  // extern "C"

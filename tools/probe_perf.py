@@ -11,6 +11,9 @@ ap.add_argument("--threads", type=int, default=0)
 ap.add_argument("--slots", type=int, default=0)
 ap.add_argument("--near", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--hot", type=int, default=-1)
+ap.add_argument("--prof", action="store_true")
+ap.add_argument("--param", action="append", default=[], help="name=value")
 a = ap.parse_args()
 t = time.time()
 if a.graph.startswith("rmat"):
@@ -24,7 +27,10 @@ elif a.graph.startswith("grid"):
 g = W.build_csr(el)
 print(f"graph {a.graph} n={g.n} m={g.m} built in {time.time()-t:.1f}s", flush=True)
 gg = W.GpuGraph(g, 0)
-gg.set_tuning(a.threads, a.slots, a.near)
+gg.set_tuning(a.threads, a.slots, a.near, a.hot)
+if a.prof: gg.set_profiling(True)
+for kv in a.param:
+    k_, v_ = kv.split('='); gg.set_param(k_, int(v_))
 print(gg.info(), flush=True)
 src = W.sample_sources(g.n, a.k, 1)
 for rep in range(a.reps):
@@ -32,3 +38,10 @@ for rep in range(a.reps):
     st = gg.last_run_stats()
     print(f"rep {rep}: {r.elapsed*1e3:.1f} ms for {len(src)} sources -> {g.m*len(src)/r.elapsed/1e9:.2f} GTEPS; "
           f"{r.elapsed/len(src)*1e3:.3f} ms/src; stats {st}; depth mean {r.depth_per_source[src].mean():.1f}", flush=True)
+    if a.prof:
+        pc = gg.profile_counters(); k = len(src)
+        print("  per source: " + ", ".join(f"{kk}={v/k:.4g}" for kk, v in pc.items()) + f"  (2m={2*g.m})", flush=True)
+        cyc = {kk: v for kk, v in pc.items() if kk.startswith("cyc_")}
+        tot = sum(cyc.values()) or 1
+        print("  phase share: " + ", ".join(f"{kk[4:]}={100*v/tot:.1f}%" for kk, v in cyc.items()) +
+              f"; per-CTA ms/source at 1.9GHz = {tot/k/1.9e6:.2f}", flush=True)
