@@ -442,9 +442,9 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
       }
     }
   });
-  // Near-window width: about half the mean minimum incident weight balances
+  // Near-window width: about a third of the mean minimum incident weight balances
   // near rescans against far refills.
-  g->near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 2.0 + 0.5))
+  g->near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 3.0 + 0.5))
                            : 1;
 
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
