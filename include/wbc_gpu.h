@@ -88,6 +88,24 @@ int wbc_gpu_bc_device(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k,
 int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* sigma,
                       double* delta, uint32_t* depth);
 
+/* Level structure of one source, for the reference's level invariants
+ * (test_engine.cpp:266-302: TraversalState::order / level_ends,
+ * engine.hpp:49-65).  order[n] receives the settlement order in caller ids
+ * (entries past *order_len are untouched), level_ends[n+1] the Eq. 4 level
+ * boundaries (level L = order[level_ends[L], level_ends[L+1])),
+ * *levels = depth.  Within a level the GPU's order is unspecified; compare
+ * levels as sets. */
+/* Test introspection: the shortest-path DAG edges one source recorded, per
+ * level (pred[i] -> succ[i] in caller ids; level L's edges are
+ * [dag_ends[L], dag_ends[L+1])).  pred/succ need room for 2m entries,
+ * dag_ends for n+1.  *levels = depth; *overflow = 1 if the per-source DAG
+ * buffer overflowed (the row-scan fallback then ran instead). */
+int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t* succ,
+                     uint32_t* dag_ends, uint32_t* levels, uint32_t* overflow);
+
+int wbc_gpu_sssp_levels(wbc_gpu_graph* g, uint32_t source, uint32_t* order, uint32_t* order_len,
+                        uint32_t* level_ends, uint32_t* levels);
+
 /* Introspection for benches/tests.  Any pointer may be NULL. */
 int wbc_gpu_graph_info(wbc_gpu_graph* g, uint32_t* n, uint32_t* m, uint32_t* max_weight,
                        int* packed_slots, uint32_t* near_width, uint64_t* graph_bytes);

@@ -436,6 +436,29 @@ class GpuGraph:
             _raise(rc)
         return dict(dist=dist, sigma=sigma, delta=delta, depth=depth.value)
 
+    def dag(self, s: int):
+        """Recorded DAG edges per level (wbc_gpu_sssp_dag): list of (pred, succ) arrays, overflow flag."""
+        n, m = self.n, self.m
+        pred = np.zeros(max(2 * m, 1), np.uint32)
+        succ = np.zeros(max(2 * m, 1), np.uint32)
+        ends = np.zeros(n + 2, np.uint32)
+        nl, ov = C.c_uint32(), C.c_uint32()
+        rc = L.load().wbc_gpu_sssp_dag(self._h, s, _p(pred), _p(succ), _p(ends), C.byref(nl), C.byref(ov))
+        if rc:
+            _raise(rc)
+        return [(pred[ends[i]:ends[i + 1]], succ[ends[i]:ends[i + 1]]) for i in range(nl.value)], bool(ov.value)
+
+    def levels(self, s: int) -> list:
+        """Eq. 4 levels of one source as sorted id arrays (wbc_gpu_sssp_levels)."""
+        n = self.n
+        order = np.zeros(max(n, 1), np.uint32)
+        ends = np.zeros(n + 2, np.uint32)
+        olen, nl = C.c_uint32(), C.c_uint32()
+        rc = L.load().wbc_gpu_sssp_levels(self._h, s, _p(order), C.byref(olen), _p(ends), C.byref(nl))
+        if rc:
+            _raise(rc)
+        return [np.sort(order[ends[i]:ends[i + 1]]) for i in range(nl.value)]
+
 
 def bc_parallel(g: CsrGraph, opt: Optional[EngineOptions] = None) -> BcResult:
     """Drop-in for wbc::bc_parallel (engine.hpp:122-130) running on the GPU."""

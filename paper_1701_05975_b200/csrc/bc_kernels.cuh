@@ -103,6 +103,13 @@ struct Workspace {
   uint32_t* far_q;       // pending with d >= F at insertion (may hold stale ids)
   uint32_t* dag_ends;    // per level: DAG edges of level L = dag[de[L], de[L+1])
   uint2* dag;            // (slot of v's row pointing at predecessor u, v)
+  // team kernel only (bc_team.cuh): per order position the distance, row
+  // start and running edge prefix; second near/far buffers (ping-pong)
+  uint32_t* ord_d;
+  uint32_t* ord_row;
+  uint32_t* epref;
+  uint32_t* near_q2;
+  uint32_t* far_q2;
   uint64_t n_stride;
   uint64_t dag_cap;
 };

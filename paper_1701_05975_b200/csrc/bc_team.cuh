@@ -1,0 +1,578 @@
+// bc_team.cuh -- the per-source Brandes pipeline run by a TEAM of C CTAs (one
+// thread-block cluster) per source.
+//
+// Why teams: with one CTA per source, 148 sources are in flight and their
+// distance arrays (4n bytes each: 2.6 MB at R-MAT-20, 388 MB together) cannot
+// stay in the 126 MB L2, so every random dist[u] gather of the relax misses to
+// HBM (ncu: 2.0 GB of DRAM traffic per source against 1.27 GB algorithmic,
+// 32% L2 hit rate).  A cluster of C CTAs working on ONE source divides the
+// number of in-flight sources by C (C = 8: 18 sources, 47 MB of distances),
+// so the gathers hit L2 and HBM only streams the CSR slots.
+//
+// Same semantics and round structure as bc_sources_kernel (bc_kernels.cuh,
+// reference engine.cpp:118-222 and :183-212); what changes is the
+// decomposition:
+//  * settle appends each settled vertex to the order together with its
+//    distance, row start and the running edge prefix (a warp scan plus one
+//    packed 64-bit atomicAdd per warp hands out (position, edge offset)
+//    pairs), so the next relax splits the level's EDGES evenly across the C
+//    CTAs without a scan, and stages its rows with coalesced loads;
+//  * sigma is pulled with one fire-and-forget global fp64 RED per DAG edge
+//    (a hub row may be split between CTAs; the sums are integer-valued, hence
+//    exact in any order), and the relax issues the atomicMin, min-weight and
+//    sigma accesses of all its unrolled groups before consuming any of them;
+//    queue appends are ballot-aggregated, one atomic per queue per warp step;
+//  * the near/far queues are ping-pong buffers (in-place compaction across
+//    CTAs would race);
+//  * team scalars (queue append counters, Delta minima, the next source
+//    index) live in a ring of 4 slots in rank 0's shared memory (DSMEM):
+//    phase p appends/reduces into slot p%4, every thread reads slot p%4 right
+//    after the barrier that ends phase p, and slot (p+2)%4 is cleared during
+//    phase p -- its last readers finished before that phase began, and its
+//    next writers start after the next barrier.  Queue lengths are therefore
+//    team-uniform registers (base + appended count), never reset in place.
+// C == 1 degenerates to one CTA with __syncthreads() as the team barrier.
+#pragma once
+
+#include "bc_kernels.cuh"
+
+namespace wbc_dev {
+
+struct TeamRed {
+  unsigned long long ord;  // settle: (count << 32) | edges appended to the order
+  unsigned long long src;  // next source index (fetched by the leader)
+  uint32_t near_app, far_app, dag_app, keep_app;
+  uint32_t min1, min2;
+  uint32_t flags;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ void team_red_reset(TeamRed& r) {
+  r.ord = 0;
+  r.near_app = r.far_app = r.dag_app = r.keep_app = 0;
+  r.min1 = r.min2 = kInfDist;
+  r.flags = 0;
+}
+
+template <int T>
+struct TeamShared {
+  uint32_t v[T];
+  uint32_t dv[T];
+  uint32_t rowadj[T];  // row start + chunk base - first edge (mod 2^32)
+  uint32_t pref[T + 1];
+  double acc[T];
+  TeamRed ring[4];     // used through rank 0's copy
+  uint32_t bcast;
+};
+
+// Warp-aggregated append to a (possibly remote) counter; returns the slot.
+__device__ __forceinline__ uint32_t team_append(uint32_t* counter) {
+  cg::coalesced_group grp = cg::coalesced_threads();
+  uint32_t base = 0;
+  if (grp.thread_rank() == 0) base = atomicAdd(counter, grp.size());
+  base = grp.shfl(base, 0);
+  return base + grp.thread_rank();
+}
+
+__device__ __forceinline__ void team_min(uint32_t v, uint32_t* target) {
+  v = __reduce_min_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && v != kInfDist) atomicMin(target, v);
+}
+
+// Largest j in [lo, hi) with key[j] <= x (key non-decreasing, key[lo] <= x),
+// found by the whole CTA with T-ary sampling: ceil(log_T(hi-lo)) rounds of
+// one coalesced load + one __syncthreads_count.
+template <int T>
+__device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo, uint32_t hi, uint32_t x) {
+  while (hi - lo > 1) {
+    const uint32_t len = hi - lo;
+    const uint32_t q = lo + static_cast<uint32_t>((static_cast<uint64_t>(len) * threadIdx.x) / T);
+    const int ok = __ldcg(key + q) <= x;
+    const int c = __syncthreads_count(ok);  // >= 1: sample 0 is lo
+    const uint32_t t = static_cast<uint32_t>(c - 1);
+    const uint32_t nlo = lo + static_cast<uint32_t>((static_cast<uint64_t>(len) * t) / T);
+    const uint32_t nhi = (t + 1 < T) ? lo + static_cast<uint32_t>((static_cast<uint64_t>(len) * (t + 1)) / T) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+template <int T, int C, bool PACKED, bool PROF>
+__global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
+  __shared__ TeamShared<T> sh;
+  const GraphView& g = p.g;
+  const int tid = threadIdx.x;
+  uint32_t rank = 0;
+  TeamRed* ring = sh.ring;
+  if constexpr (C > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    rank = cl.block_rank();
+    ring = cl.map_shared_rank(sh.ring, 0);
+  }
+  const bool leader = rank == 0 && tid == 0;
+  const uint32_t team = blockIdx.x / C;
+  const uint64_t off = static_cast<uint64_t>(team) * p.ws.n_stride;
+  const uint64_t keep_pol = l2_policy_evict_last();
+  const uint64_t stream_pol = l2_policy_evict_first();
+  const DistView dist{nullptr, p.ws.dist + off, 0, p.l2hot, keep_pol};
+  double* const sigma = p.ws.sigma + off;
+  double* const delta = p.ws.delta + off;
+  uint32_t* const order = p.ws.order + off;
+  uint32_t* const ord_d = p.ws.ord_d + off;
+  uint32_t* const ord_row = p.ws.ord_row + off;
+  uint32_t* const epref = p.ws.epref + off;
+  uint32_t* const lev = p.ws.level_ends + off;
+  uint32_t* const nq[2] = {p.ws.near_q + off, p.ws.near_q2 + off};
+  uint32_t* const fq[2] = {p.ws.far_q + off, p.ws.far_q2 + off};
+  uint32_t* const dag_ends = p.ws.dag_ends + off;
+  uint2* const dag = p.ws.dag + static_cast<uint64_t>(team) * p.ws.dag_cap;
+  const uint32_t dag_cap = static_cast<uint32_t>(p.ws.dag_cap);
+  const uint32_t n = g.n;
+  const uint32_t S = p.near_width;
+  constexpr uint32_t TT = static_cast<uint32_t>(T) * C;  // team threads
+  const uint32_t gtid = rank * T + tid;                 // team thread id
+
+  unsigned long long c_relax = 0, c_near = 0, c_far = 0, c_refill = 0, c_impr = 0;
+  unsigned long long t_last = 0, t_phase[5] = {0, 0, 0, 0, 0};
+  const bool timing = PROF && leader;
+  auto tick = [&](int k) {
+    if (timing) {
+      const unsigned long long t = clock64();
+      t_phase[k] += t - t_last;
+      t_last = t;
+    }
+  };
+
+  uint32_t ph = 0;
+  auto tsync = [&]() {
+    if constexpr (C == 1)
+      __syncthreads();
+    else
+      cg::this_cluster().sync();
+    ++ph;
+    if (leader) team_red_reset(ring[(ph + 2) & 3]);
+  };
+  auto cur = [&]() -> TeamRed& { return ring[ph & 3]; };
+  auto prev = [&]() -> TeamRed& { return ring[(ph - 1) & 3]; };
+
+  if (tid == 0 && rank == 0) {
+    for (int k = 0; k < 4; ++k) team_red_reset(sh.ring[k]);
+    sh.ring[0].src = atomicAdd(p.counter, 1ULL);
+  }
+
+  // Stages the edges [cb, my_e) of the level's vertices starting at order
+  // position j (edge prefix epref, vertices j.. have epref < my_e) into
+  // shared memory; returns the chunk's vertex count and sets ce.
+  auto stage = [&](uint32_t j, uint32_t fe, uint32_t cb, uint32_t my_e, uint32_t Ee, uint32_t& ce) -> int {
+    const uint32_t jt = j + tid;
+    uint32_t gs = Ee;
+    if (jt < fe) gs = __ldcg(epref + jt);
+    const bool use = jt < fe && gs < my_e;
+    if (use) {
+      sh.v[tid] = __ldcg(order + jt);
+      sh.dv[tid] = __ldcg(ord_d + jt);
+      sh.rowadj[tid] = __ldcg(ord_row + jt) + cb - gs;
+      sh.pref[tid] = (gs > cb ? gs : cb) - cb;
+      sh.acc[tid] = 0.0;
+    }
+    if (tid == T - 1) sh.bcast = (j + T < fe) ? __ldcg(epref + j + T) : Ee;
+    const int cnt = __syncthreads_count(use);
+    const uint32_t nxt = sh.bcast;
+    ce = (cnt < T) ? my_e : min(nxt, my_e);
+    if (tid == 0) sh.pref[cnt] = ce - cb;
+    __syncthreads();
+    return cnt;
+  };
+
+  for (;;) {
+    tsync();
+    const unsigned long long idx = prev().src;
+    if (idx >= p.k) break;
+    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(idx);
+    const uint32_t s = __ldg(p.inv + s_orig);
+    if (timing) t_last = clock64();
+
+    // ---- init_state (engine.cpp:118-142): d = inf except d[s] = 0, level 0 = {s}
+    for (uint32_t i = gtid; i < n; i += TT) dist.gl[i] = (i == s) ? 0u : kInfDist;
+    const uint32_t s_row = __ldg(g.offsets + s);
+    const uint32_t s_deg = __ldg(g.offsets + s + 1) - s_row;
+    if (leader) {
+      order[0] = s;
+      ord_d[0] = 0;
+      ord_row[0] = s_row;
+      epref[0] = 0;
+      sigma[s] = 1.0;
+      delta[s] = 0.0;
+      lev[0] = 0;
+      lev[1] = 1;
+      dag_ends[0] = 0;
+    }
+    // team-uniform registers
+    uint32_t fb = 0, fe = 1, nlev = 1, ord_len = 1, ord_edges = s_deg, Eb = 0, Ee = s_deg;
+    uint32_t near_len = 0, far_len = 0, dag_len = 0;
+    int nc = 0, fc = 0;
+    uint64_t F = S;
+    uint32_t kept_min = kInfDist;
+    bool dag_over = false;
+    tsync();
+    tick(0);
+
+    for (;;) {
+      // ---------------- relax level nlev-1, pull its sigma, record DAG edges
+      {
+        TeamRed& R = cur();
+        uint32_t kmin = kInfDist;
+        bool over = false;
+        const uint32_t Fu = F >= kInfDist ? kInfDist : static_cast<uint32_t>(F);
+        const uint32_t E = Ee - Eb;
+        const uint32_t my_b = Eb + static_cast<uint32_t>((static_cast<uint64_t>(E) * rank) / C);
+        const uint32_t my_e = Eb + static_cast<uint32_t>((static_cast<uint64_t>(E) * (rank + 1)) / C);
+        c_relax += (rank == 0) ? E : 0;
+        if (my_b < my_e) {
+          uint32_t j = block_find<T>(epref, fb, fe, my_b);
+          uint32_t cb = my_b;
+          while (cb < my_e) {
+            uint32_t ce;
+            const int cnt = stage(j, fe, cb, my_e, Ee, ce);
+            const uint32_t total = ce - cb;
+            uint32_t wb, we;
+            if (warp_range<T>(total, wb, we)) {
+              int j0 = find_row(sh.pref, cnt, wb);
+              const uint32_t lane = tid & 31;
+              const uint32_t lt = (1u << lane) - 1u;
+              for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
+                // A: rows and slots of kUnroll groups of 32 edges
+                int jj[kUnroll];
+                uint32_t slot[kUnroll], uu[kUnroll], nd[kUnroll], du[kUnroll], dvv[kUnroll];
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                  const uint32_t eg = e0 + 32 * k;
+                  jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0) : 0;
+                  const uint32_t e = eg + lane;
+                  slot[k] = e < we ? sh.rowadj[jj[k]] + e : 0xFFFFFFFFu;
+                }
+                // B, C: slot stream, then the distance gathers
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                  uint32_t w = 0;
+                  uu[k] = 0;
+                  if (slot[k] != 0xFFFFFFFFu) load_slot<PACKED>(g, slot[k], uu[k], w, stream_pol);
+                  dvv[k] = sh.dv[jj[k]];
+                  nd[k] = dvv[k] + w;
+                }
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) du[k] = slot[k] != 0xFFFFFFFFu ? dist.load(uu[k]) : 0u;
+                // D: every dependent access of the kUnroll groups in flight at once
+                bool pr[kUnroll], im[kUnroll];
+                uint32_t old[kUnroll], mw[kUnroll];
+                double sg[kUnroll];
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                  const bool valid = slot[k] != 0xFFFFFFFFu;
+                  // u precedes v on a shortest path: d[u] + w == d[v]  (nd - dv == w)
+                  pr[k] = valid && du[k] != kInfDist && du[k] + (nd[k] - dvv[k]) == dvv[k];
+                  im[k] = valid && nd[k] < du[k];
+                }
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) old[k] = im[k] ? dist.fetch_min(uu[k], nd[k]) : kInfDist;
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) mw[k] = (im[k] && nd[k] < Fu) ? __ldg(g.minw + uu[k]) : 0u;
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) sg[k] = pr[k] ? __ldcg(sigma + uu[k]) : 0.0;
+                // E: consume.  Delta candidates need no atomic result: a lane
+                // that lost the race recorded a key >= the winner's.
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k)
+                  if (im[k] && nd[k] < Fu) kmin = min(kmin, nd[k] + mw[k]);
+                // sigma pull: fire-and-forget fp64 RED (integer-valued: exact in any order)
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k)
+                  if (pr[k]) atomicAdd(sigma + sh.v[jj[k]], sg[k]);
+                // appends: one ballot-aggregated atomic per queue per warp iteration
+                uint32_t bd[kUnroll], bn[kUnroll], bf[kUnroll];
+                uint32_t cd = 0, cn = 0, cf = 0;
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                  const bool imp = im[k] && nd[k] < old[k];
+                  c_impr += imp;
+                  bd[k] = __ballot_sync(0xffffffffu, pr[k]);
+                  bn[k] = __ballot_sync(0xffffffffu, imp && nd[k] < Fu && old[k] >= Fu);
+                  bf[k] = __ballot_sync(0xffffffffu, imp && nd[k] >= Fu && old[k] == kInfDist);
+                  cd += __popc(bd[k]);
+                  cn += __popc(bn[k]);
+                  cf += __popc(bf[k]);
+                }
+                if (cd | cn | cf) {
+                  uint32_t base_d = 0, base_n = 0, base_f = 0;
+                  if (lane == 0) {
+                    if (cd) base_d = atomicAdd(&R.dag_app, cd);
+                    if (cn) base_n = atomicAdd(&R.near_app, cn);
+                    if (cf) base_f = atomicAdd(&R.far_app, cf);
+                  }
+                  base_d = dag_len + __shfl_sync(0xffffffffu, base_d, 0);
+                  base_n = near_len + __shfl_sync(0xffffffffu, base_n, 0);
+                  base_f = far_len + __shfl_sync(0xffffffffu, base_f, 0);
+#pragma unroll
+                  for (int k = 0; k < kUnroll; ++k) {
+                    if (bd[k] >> lane & 1u) {
+                      const uint32_t pos = base_d + __popc(bd[k] & lt);
+                      if (pos < dag_cap)
+                        dag[pos] = make_uint2(slot[k], sh.v[jj[k]]);
+                      else
+                        over = true;
+                    }
+                    if (bn[k] >> lane & 1u) nq[nc][base_n + __popc(bn[k] & lt)] = uu[k];
+                    if (bf[k] >> lane & 1u) fq[fc][base_f + __popc(bf[k] & lt)] = uu[k];
+                    base_d += __popc(bd[k]);
+                    base_n += __popc(bn[k]);
+                    base_f += __popc(bf[k]);
+                  }
+                }
+              }
+            }
+            __syncthreads();  // staged chunk fully consumed
+            j += cnt;
+            cb = ce;
+          }
+        }
+        team_min(kmin, &R.min1);
+        if (over) R.flags = 1;
+      }
+      tsync();
+      uint32_t thr;
+      {
+        TeamRed& Q = prev();
+        near_len += Q.near_app;
+        far_len += Q.far_app;
+        dag_len += Q.dag_app;
+        thr = min(kept_min, Q.min1);
+        dag_over = dag_over || Q.flags;
+      }
+      if (leader) dag_ends[nlev] = dag_len;
+      tick(1);
+
+      // ---------------- threshold: make the near-only Delta exact
+      bool done = (near_len == 0 && far_len == 0);
+      uint64_t far_min = kInfDist;
+      while (!done && thr > F) {
+        uint64_t F_new = F + S;
+        if (far_min != kInfDist) {
+          const uint64_t jump = far_min + S < thr ? far_min + S : static_cast<uint64_t>(thr);
+          if (jump > F_new) F_new = jump;
+        }
+        const uint32_t Fo = F >= kInfDist ? kInfDist : static_cast<uint32_t>(F);
+        const uint32_t Fn = F_new >= kInfDist ? kInfDist : static_cast<uint32_t>(F_new);
+        TeamRed& R = cur();
+        uint32_t lkey = kInfDist, lfar = kInfDist;
+        c_far += (rank == 0) ? far_len : 0;
+        c_refill += (rank == 0) ? 1 : 0;
+        const uint32_t* src = fq[fc];
+        uint32_t* dst = fq[fc ^ 1];
+        for (uint32_t i = gtid; i < far_len; i += TT) {
+          const uint32_t u = __ldcg(src + i);
+          const uint32_t du = dist.load(u);
+          if (du >= Fo) {  // du < Fo: already near or settled
+            if (du < Fn) {
+              nq[nc][near_len + team_append(&R.near_app)] = u;
+              lkey = min(lkey, du + __ldg(g.minw + u));
+            } else {
+              dst[team_append(&R.far_app)] = u;
+              lfar = min(lfar, du);
+            }
+          }
+        }
+        team_min(lkey, &R.min1);
+        team_min(lfar, &R.min2);
+        tsync();
+        {
+          TeamRed& Q = prev();
+          near_len += Q.near_app;
+          far_len = Q.far_app;
+          fc ^= 1;
+          thr = min(thr, Q.min1);
+          far_min = Q.min2;
+        }
+        F = F_new;
+        done = (near_len == 0 && far_len == 0);
+      }
+      tick(2);
+      if (done) break;
+
+      // ---------------- settle: d < Delta joins level nlev, with its row data
+      {
+        TeamRed& R = cur();
+        uint32_t lkept = kInfDist;
+        c_near += (rank == 0) ? near_len : 0;
+        const uint32_t* src = nq[nc];
+        uint32_t* dst = nq[nc ^ 1];
+        const uint32_t sb = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * rank) / C);
+        const uint32_t se = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * (rank + 1)) / C);
+        // warp-level: each warp scans 32 entries, one packed atomic hands out
+        // (order position, edge offset) for its settled lanes; no CTA barrier
+        const uint32_t lane = tid & 31;
+        for (uint32_t c = sb + (tid & ~31u); c < se; c += T) {
+          const uint32_t i = c + lane;
+          uint32_t u = 0, du = kInfDist, row = 0, deg = 0;
+          const bool have = i < se;
+          if (have) {
+            u = __ldcg(src + i);
+            du = dist.load(u);
+          }
+          const bool st = have && du < thr;
+          if (st) {
+            row = __ldg(g.offsets + u);
+            deg = __ldg(g.offsets + u + 1) - row;
+          }
+          const uint32_t bs = __ballot_sync(0xffffffffu, st);
+          if (bs) {
+            uint32_t pe = deg;  // inclusive warp scan of degrees
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, pe, o);
+              if (lane >= static_cast<uint32_t>(o)) pe += y;
+            }
+            const uint32_t wtot = __shfl_sync(0xffffffffu, pe, 31);
+            unsigned long long base = 0;
+            if (lane == 0) base = atomicAdd(&R.ord, (static_cast<unsigned long long>(__popc(bs)) << 32) | wtot);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (st) {
+              const uint32_t pos = ord_len + static_cast<uint32_t>(base >> 32) + __popc(bs & ((1u << lane) - 1u));
+              order[pos] = u;
+              ord_d[pos] = du;
+              ord_row[pos] = row;
+              epref[pos] = ord_edges + static_cast<uint32_t>(base) + (pe - deg);
+              sigma[u] = 0.0;
+              delta[u] = 0.0;
+            }
+          }
+          const uint32_t bk = __ballot_sync(0xffffffffu, have && !st);
+          if (bk) {
+            uint32_t kb = 0;
+            if (lane == 0) kb = atomicAdd(&R.keep_app, __popc(bk));
+            kb = __shfl_sync(0xffffffffu, kb, 0);
+            if (have && !st) {
+              dst[kb + __popc(bk & ((1u << lane) - 1u))] = u;
+              lkept = min(lkept, du + __ldg(g.minw + u));
+            }
+          }
+        }
+        team_min(lkept, &R.min1);
+      }
+      tsync();
+      {
+        TeamRed& Q = prev();
+        fb = ord_len;
+        ord_len += static_cast<uint32_t>(Q.ord >> 32);
+        fe = ord_len;
+        Eb = ord_edges;
+        ord_edges += static_cast<uint32_t>(Q.ord);
+        Ee = ord_edges;
+        near_len = Q.keep_app;
+        nc ^= 1;
+        kept_min = Q.min1;
+        ++nlev;
+      }
+      if (leader) lev[nlev] = ord_len;
+      tick(3);
+    }
+
+    // ---------------- dependency accumulation, deepest level first
+    if (!dag_over) {
+      for (uint32_t L = nlev - 1; L >= 1; --L) {
+        // dag_ends[nlev] is written by the leader in this very phase: use the register
+        const uint32_t b = __ldcg(dag_ends + L), e = L + 1 == nlev ? dag_len : __ldcg(dag_ends + L + 1);
+        for (uint32_t i = b + gtid; i < e; i += TT) {
+          const uint2 d = __ldcg(dag + i);
+          uint32_t u, w;
+          load_slot<PACKED>(g, d.x, u, w);
+          const uint32_t v = d.y;
+          // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
+          const double c = __ldcg(sigma + u) / __ldcg(sigma + v) * (1.0 + __ldcg(delta + v));
+          atomicAdd(delta + u, c);
+          if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + d.x), c);
+        }
+        // level L's delta is final (levels > L were done in earlier phases)
+        const uint32_t vb = __ldcg(lev + L), ve = L + 1 == nlev ? ord_len : __ldcg(lev + L + 1);
+        for (uint32_t q = vb + gtid; q < ve; q += TT) {
+          const uint32_t w = __ldcg(order + q);
+          atomicAdd(p.node_bc + w, __ldcg(delta + w));
+        }
+        tsync();
+      }
+    } else {
+      // Row-scan pull fallback (the reference's loop shape) when the DAG
+      // buffer overflowed: phase L computes delta of level L from its rows
+      // and adds the (final) delta of level L+1 to node BC.
+      if (leader) atomicAdd(p.overflow, 1u);
+      for (int L = static_cast<int>(nlev) - 1; L >= 0; --L) {
+        const uint32_t pb = __ldcg(lev + L), pe = static_cast<uint32_t>(L) + 1 == nlev ? ord_len : __ldcg(lev + L + 1);
+        const uint32_t lEb = __ldcg(epref + pb);
+        const uint32_t lEe = pe < ord_len ? __ldcg(epref + pe) : ord_edges;
+        const uint32_t E = lEe - lEb;
+        const uint32_t my_b = lEb + static_cast<uint32_t>((static_cast<uint64_t>(E) * rank) / C);
+        const uint32_t my_e = lEb + static_cast<uint32_t>((static_cast<uint64_t>(E) * (rank + 1)) / C);
+        if (my_b < my_e) {
+          uint32_t j = block_find<T>(epref, pb, pe, my_b);
+          uint32_t cb = my_b;
+          while (cb < my_e) {
+            uint32_t ce;
+            const int cnt = stage(j, pe, cb, my_e, lEe, ce);
+            expand_edges<T>(sh.pref, cnt, ce - cb, [&](uint32_t e, int jl) {
+              const uint32_t slot = sh.rowadj[jl] + e;
+              uint32_t x, w;
+              load_slot<PACKED>(g, slot, x, w);
+              const uint32_t dx = dist.load(x);
+              if (dx != kInfDist && dx == sh.dv[jl] + w) {
+                const uint32_t wv = sh.v[jl];
+                const double c2 = __ldcg(sigma + wv) / __ldcg(sigma + x) * (1.0 + __ldcg(delta + x));
+                atomicAdd(&sh.acc[jl], c2);
+                if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + slot), c2);
+              }
+            });
+            __syncthreads();
+            if (tid < cnt && sh.acc[tid] != 0.0) atomicAdd(delta + sh.v[tid], sh.acc[tid]);
+            __syncthreads();
+            j += cnt;
+            cb = ce;
+          }
+        }
+        if (static_cast<uint32_t>(L) + 1 < nlev) {
+          const uint32_t vb = __ldcg(lev + L + 1), ve = static_cast<uint32_t>(L) + 2 == nlev ? ord_len : __ldcg(lev + L + 2);
+          for (uint32_t q = vb + gtid; q < ve; q += TT) {
+            const uint32_t w = __ldcg(order + q);
+            atomicAdd(p.node_bc + w, __ldcg(delta + w));
+          }
+        }
+        tsync();
+      }
+    }
+    tick(4);
+    if (leader) {
+      if (p.depth) p.depth[s_orig] = nlev;
+      cur().src = atomicAdd(p.counter, 1ULL);
+    }
+    if (PROF && leader) {
+      atomicAdd(p.prof + kProfRounds, nlev);
+      atomicAdd(p.prof + kProfDagEdges, dag_len);
+      atomicAdd(p.prof + kProfRelaxSlots, c_relax);
+      atomicAdd(p.prof + kProfNearScanned, c_near);
+      atomicAdd(p.prof + kProfFarScanned, c_far);
+      atomicAdd(p.prof + kProfRefills, c_refill);
+      for (int k = 0; k < 5; ++k) {
+        atomicAdd(p.prof + kProfCyclesInit + k, t_phase[k]);
+        t_phase[k] = 0;
+      }
+      c_relax = c_near = c_far = c_refill = 0;
+    }
+    if (PROF) {
+      c_impr = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(c_impr));
+      if ((tid & 31) == 0) atomicAdd(p.prof + kProfImprovements, c_impr);
+      c_impr = 0;
+    }
+  }
+  // no CTA may leave while others can still touch its shared memory
+  if constexpr (C > 1) cg::this_cluster().sync();
+}
+
+}  // namespace wbc_dev

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -23,6 +24,7 @@
 #include <vector>
 
 #include "bc_kernels.cuh"
+#include "bc_team.cuh"
 #include "wbc_gpu.h"
 
 namespace {
@@ -120,6 +122,8 @@ struct wbc_gpu_graph {
   int tune_slots = 0;
   int64_t tune_hot = -1;
   int64_t tune_l2hot = -1;
+  int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
+  bool ws_team = false;        // workspace carries the team-kernel arrays
   bool profiling = false;
   uint64_t stats[4] = {0, 0, 0, 0};
   uint64_t prof_host[wbc_dev::kProfCounters] = {};
@@ -152,7 +156,25 @@ KernelFn pick_kernel(int threads, bool packed, bool prof = false) {
   return prof ? pick_kernel_t<false, true>(threads) : pick_kernel_t<false, false>(threads);
 }
 
+template <bool PACKED, bool PROF>
+KernelFn pick_team_t(int c) {
+  using namespace wbc_dev;
+  switch (c) {
+    case 1: return bc_team_kernel<1024, 1, PACKED, PROF>;
+    case 2: return bc_team_kernel<1024, 2, PACKED, PROF>;
+    case 4: return bc_team_kernel<1024, 4, PACKED, PROF>;
+    case 8: return bc_team_kernel<1024, 8, PACKED, PROF>;
+    default: return bc_team_kernel<1024, 16, PACKED, PROF>;
+  }
+}
+
+KernelFn pick_team(int c, bool packed, bool prof = false) {
+  if (packed) return prof ? pick_team_t<true, true>(c) : pick_team_t<true, false>(c);
+  return prof ? pick_team_t<false, true>(c) : pick_team_t<false, false>(c);
+}
+
 struct LaunchShape {
+  int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
   int threads = 128;
   uint32_t hot = 0;        // vertices with shared-memory distances
   uint32_t l2hot = 0;      // vertices whose distance accesses carry an evict-last hint
@@ -173,6 +195,22 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   LaunchShape s;
   const uint64_t n = g->n;
   const bool tiny = n * 4 <= 24 * 1024;
+  if (g->tune_cluster > 0) {
+    s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
+              : g->tune_cluster <= 8 ? 8 : 16;
+    s.threads = 1024;
+    return s;
+  }
+  // Skewed graphs run on the team kernel (bc_team.cuh).  One CTA per source
+  // while 148 distance arrays fit in half of L2 (BA-65536: 24.4 vs 18.0
+  // GTEPS for the per-CTA kernel), else two-CTA clusters, halving the
+  // in-flight distance footprint (R-MAT-20: 37.1 vs 34.4; C=4 strands 16
+  // SMs, 36.3).  Measured on B200, DESIGN.md §4.
+  if (g->tune_cluster < 0 && !tiny && g->hot_coverage_25k >= 0.4) {
+    s.cluster = n * 4 * static_cast<uint64_t>(g->sm_count) <= (64ULL << 20) ? 1 : 2;
+    s.threads = 1024;
+    return s;
+  }
   if (g->tune_threads)
     s.threads = g->tune_threads <= 128 ? 128 : g->tune_threads <= 256 ? 256 : g->tune_threads <= 512 ? 512 : 1024;
   else if (!tiny && g->hot_coverage_25k >= 0.4)
@@ -208,27 +246,53 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   const uint64_t ns = round_up(uint64_t{g->n} + 2, 64);
   const uint64_t dag_cap = round_up(uint64_t{g->n} + uint64_t{g->n} / 2 + 1024, 64);
-  const uint64_t per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4) + dag_cap * 8;
-  const KernelFn fn = pick_kernel(shape.threads, g->packed);
-  for (const bool prof : {false, true})
-    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(shape.dyn_smem)));
-  int per_sm = 0;
-  WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, reinterpret_cast<const void*>(fn), shape.threads, shape.dyn_smem));
-  if (per_sm < 1) return set_error(WBC_E_CUDA, "kernel does not fit on an SM with this launch shape");
-  int slots = per_sm * g->sm_count;
+  const bool team = shape.cluster > 0;
+  const uint64_t per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? 20 : 0)) + dag_cap * 8;
+  int slots = 0;
+  if (team) {
+    for (const bool prof : {false, true}) {
+      const void* f = reinterpret_cast<const void*>(pick_team(shape.cluster, g->packed, prof));
+      if (shape.cluster > 8)
+        WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    }
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = shape.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(shape.cluster * g->sm_count, 1, 1);
+    cfg.blockDim = dim3(shape.threads, 1, 1);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    WBC_CUDA_TRY(cudaOccupancyMaxActiveClusters(
+        &clusters, reinterpret_cast<const void*>(pick_team(shape.cluster, g->packed)), &cfg));
+    if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
+    slots = clusters;
+  } else {
+    const KernelFn fn = pick_kernel(shape.threads, g->packed);
+    for (const bool prof : {false, true})
+      WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(shape.dyn_smem)));
+    int per_sm = 0;
+    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(fn), shape.threads, shape.dyn_smem));
+    if (per_sm < 1) return set_error(WBC_E_CUDA, "kernel does not fit on an SM with this launch shape");
+    slots = per_sm * g->sm_count;
+  }
   if (g->tune_slots) slots = std::min(slots, g->tune_slots);
   slots = std::max(1, std::min(slots, want));
   size_t free_b = 0, total_b = 0;
   WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  uint64_t avail = free_b + (g->d_ws ? uint64_t(g->ws_slots) * per_slot : 0);
+  const uint64_t old_per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (g->ws_team ? 20 : 0)) + dag_cap * 8;
+  uint64_t avail = free_b + (g->d_ws ? uint64_t(g->ws_slots) * old_per_slot : 0);
   const uint64_t reserve = (4ULL << 30) + total_b / 10;  // 4 GiB + 10% headroom
   avail = avail > reserve ? avail - reserve : 0;
   slots = static_cast<int>(std::min<uint64_t>(slots, std::max<uint64_t>(1, avail / per_slot)));
   *slots_out = slots;
-  if (g->d_ws && g->ws_slots >= slots) return WBC_OK;
+  if (g->d_ws && g->ws_slots >= slots && (g->ws_team || !team)) return WBC_OK;
   cudaFree(g->d_ws);
   g->d_ws = nullptr;
   g->ws_slots = 0;
@@ -239,6 +303,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
                                       " bytes failed: " + cudaGetErrorString(err));
   g->d_ws = base;
   g->ws_slots = slots;
+  g->ws_team = team;
   char* p = static_cast<char*>(base);
   auto carve = [&](uint64_t bytes) {
     char* q = p;
@@ -256,6 +321,15 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   g->ws.near_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
   g->ws.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
   g->ws.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  if (team) {
+    g->ws.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    g->ws.ord_row = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    g->ws.epref = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    g->ws.near_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    g->ws.far_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  } else {
+    g->ws.ord_d = g->ws.ord_row = g->ws.epref = g->ws.near_q2 = g->ws.far_q2 = nullptr;
+  }
   return WBC_OK;
 }
 
@@ -307,12 +381,30 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_node_dev, 0, uint64_t{g->n} * 8, stream));
   if (g->profiling)
     WBC_CUDA_TRY(cudaMemsetAsync(g->d_prof, 0, sizeof(unsigned long long) * wbc_dev::kProfCounters, stream));
-  pick_kernel(shape.threads, g->packed, g->profiling)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p);
-  WBC_CUDA_TRY(cudaGetLastError());
+  if (shape.cluster > 0) {
+    // whole distance arrays of the few in-flight teams get evict-last
+    if (g->tune_l2hot < 0) p.l2hot = g->n;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = shape.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(slots * shape.cluster, 1, 1);
+    cfg.blockDim = dim3(shape.threads, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(shape.cluster, g->packed, g->profiling), p));
+  } else {
+    pick_kernel(shape.threads, g->packed, g->profiling)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p);
+    WBC_CUDA_TRY(cudaGetLastError());
+  }
   wbc_dev::scatter_add_kernel<<<launch_grid(g->n), 256, 0, stream>>>(d_node, g->d_node_dev, g->d_perm, g->n);
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
-  g->stats[1] = shape.threads;
+  g->stats[1] = shape.threads * std::max(1, shape.cluster);
   g->stats[3] = 2;
   return WBC_OK;
 }
@@ -381,6 +473,7 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
     delete g;
     return set_error(WBC_E_NOT_BUILT, "device is not sm_100 class (built for sm_100a only)");
   }
+  if (const char* e = std::getenv("WBC_GPU_CLUSTER")) g->tune_cluster = std::atoi(e);  // tuning default
   g->n = n;
   g->m = m;
   g->max_weight = static_cast<uint32_t>(maxw);
@@ -523,6 +616,7 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "near_width") g->near_width = value > 0 ? static_cast<uint32_t>(value) : g->near_width;
   else if (k == "hot") g->tune_hot = value;
   else if (k == "l2hot") g->tune_l2hot = value;
+  else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }
@@ -683,6 +777,59 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
   cudaFree(d_src);
   cudaFree(d_dep);
   return rc;
+}
+
+int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t* succ,
+                     uint32_t* dag_ends, uint32_t* levels, uint32_t* overflow) {
+  if (!g || !pred || !succ || !dag_ends || !levels || !overflow) return set_error(WBC_E_INVALID, "null argument");
+  if (source >= g->n) return set_error(WBC_E_INVALID, "init_state: source out of range");
+  uint32_t depth = 0;
+  int rc = wbc_gpu_sssp_dump(g, source, nullptr, nullptr, nullptr, &depth);
+  if (rc) return rc;
+  unsigned int ov = 0;
+  WBC_CUDA_TRY(cudaMemcpy(&ov, g->d_overflow, 4, cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> de(uint64_t{depth} + 1);
+  WBC_CUDA_TRY(cudaMemcpy(de.data(), g->ws.dag_ends, de.size() * 4, cudaMemcpyDeviceToHost));
+  const uint32_t len = std::min<uint64_t>(de[depth], g->ws.dag_cap);
+  std::vector<uint2> d(len);
+  if (len) WBC_CUDA_TRY(cudaMemcpy(d.data(), g->ws.dag, uint64_t{len} * 8, cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> slots(g->packed ? 2ULL * g->m : 0);
+  std::vector<uint2> slots64(g->packed ? 0 : 2ULL * g->m);
+  if (g->m) {
+    if (g->packed)
+      WBC_CUDA_TRY(cudaMemcpy(slots.data(), g->d_slots32, 8ULL * g->m, cudaMemcpyDeviceToHost));
+    else
+      WBC_CUDA_TRY(cudaMemcpy(slots64.data(), g->d_slots64, 16ULL * g->m, cudaMemcpyDeviceToHost));
+  }
+  for (uint32_t i = 0; i < len; ++i) {
+    const uint32_t u = g->packed ? slots[d[i].x] >> g->wbits : slots64[d[i].x].x;
+    pred[i] = g->perm[u];
+    succ[i] = g->perm[d[i].y];
+  }
+  std::memcpy(dag_ends, de.data(), de.size() * 4);
+  *levels = depth;
+  *overflow = ov;
+  return WBC_OK;
+}
+
+int wbc_gpu_sssp_levels(wbc_gpu_graph* g, uint32_t source, uint32_t* order, uint32_t* order_len,
+                        uint32_t* level_ends, uint32_t* levels) {
+  if (!g || !order || !order_len || !level_ends || !levels) return set_error(WBC_E_INVALID, "null argument");
+  if (source >= g->n) return set_error(WBC_E_INVALID, "init_state: source out of range");
+  uint32_t depth = 0;
+  int rc = wbc_gpu_sssp_dump(g, source, nullptr, nullptr, nullptr, &depth);
+  if (rc) return rc;
+  // workspace slot 0 still holds the source's order / level ends
+  std::vector<uint32_t> lev(uint64_t{depth} + 1);
+  WBC_CUDA_TRY(cudaMemcpy(lev.data(), g->ws.level_ends, lev.size() * 4, cudaMemcpyDeviceToHost));
+  const uint32_t len = lev[depth];
+  std::vector<uint32_t> ord(len);
+  if (len) WBC_CUDA_TRY(cudaMemcpy(ord.data(), g->ws.order, uint64_t{len} * 4, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < len; ++i) order[i] = g->perm[ord[i]];
+  std::memcpy(level_ends, lev.data(), lev.size() * 4);
+  *order_len = len;
+  *levels = depth;
+  return WBC_OK;
 }
 
 }  // extern "C"
