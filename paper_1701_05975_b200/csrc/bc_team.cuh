@@ -34,6 +34,8 @@
 // C == 1 degenerates to one CTA with __syncthreads() as the team barrier.
 #pragma once
 
+#include <type_traits>
+
 #include "bc_kernels.cuh"
 
 namespace wbc_dev {
@@ -74,6 +76,17 @@ __device__ __forceinline__ uint32_t team_append(uint32_t* counter) {
   return base + grp.thread_rank();
 }
 
+// Distances of a team's source: few sources are in flight, so every entry
+// carries the evict-last hint (no per-access branch).
+struct TeamDist {
+  uint32_t* gl;
+  uint64_t keep;
+  __device__ __forceinline__ uint32_t load(uint32_t u) const { return ld_cg_hint(gl + u, keep); }
+  __device__ __forceinline__ uint32_t fetch_min(uint32_t u, uint32_t v) const {
+    return atom_min_hint(gl + u, v, keep);
+  }
+};
+
 __device__ __forceinline__ void team_min(uint32_t v, uint32_t* target) {
   v = __reduce_min_sync(0xffffffffu, v);
   if ((threadIdx.x & 31) == 0 && v != kInfDist) atomicMin(target, v);
@@ -98,9 +111,16 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
   return lo;
 }
 
+// Per-warp compaction queues of the two-pass relax (dynamic shared memory):
+// 5 arrays of kTeamQ u32 per warp; a warp holds < 32 entries between drains
+// and adds at most 32 * kUnroll per step.
+constexpr uint32_t kTeamQ = 32 * kUnroll + 32;
+__host__ __device__ constexpr size_t team_dyn_smem(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
+
 template <int T, int C, bool PACKED, bool PROF>
 __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
   __shared__ TeamShared<T> sh;
+  extern __shared__ uint32_t team_q[];
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   uint32_t rank = 0;
@@ -115,7 +135,7 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
   const uint64_t off = static_cast<uint64_t>(team) * p.ws.n_stride;
   const uint64_t keep_pol = l2_policy_evict_last();
   const uint64_t stream_pol = l2_policy_evict_first();
-  const DistView dist{nullptr, p.ws.dist + off, 0, p.l2hot, keep_pol};
+  const TeamDist dist{p.ws.dist + off, keep_pol};
   double* const sigma = p.ws.sigma + off;
   double* const delta = p.ws.delta + off;
   uint32_t* const order = p.ws.order + off;
@@ -123,8 +143,10 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
   uint32_t* const ord_row = p.ws.ord_row + off;
   uint32_t* const epref = p.ws.epref + off;
   uint32_t* const lev = p.ws.level_ends + off;
-  uint32_t* const nq[2] = {p.ws.near_q + off, p.ws.near_q2 + off};
-  uint32_t* const fq[2] = {p.ws.far_q + off, p.ws.far_q2 + off};
+  uint32_t* const nq0 = p.ws.near_q + off;
+  uint32_t* const nq1 = p.ws.near_q2 + off;
+  uint32_t* const fq0 = p.ws.far_q + off;
+  uint32_t* const fq1 = p.ws.far_q2 + off;
   uint32_t* const dag_ends = p.ws.dag_ends + off;
   uint2* const dag = p.ws.dag + static_cast<uint64_t>(team) * p.ws.dag_cap;
   const uint32_t dag_cap = static_cast<uint32_t>(p.ws.dag_cap);
@@ -224,6 +246,8 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         TeamRed& R = cur();
         uint32_t kmin = kInfDist;
         bool over = false;
+        uint32_t* const nqc = nc ? nq1 : nq0;
+        uint32_t* const fqc = fc ? fq1 : fq0;
         const uint32_t Fu = F >= kInfDist ? kInfDist : static_cast<uint32_t>(F);
         const uint32_t E = Ee - Eb;
         const uint32_t my_b = Eb + static_cast<uint32_t>((static_cast<uint64_t>(E) * rank) / C);
@@ -241,10 +265,81 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
               int j0 = find_row(sh.pref, cnt, wb);
               const uint32_t lane = tid & 31;
               const uint32_t lt = (1u << lane) - 1u;
-              for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
-                // A: rows and slots of kUnroll groups of 32 edges
-                int jj[kUnroll];
-                uint32_t slot[kUnroll], uu[kUnroll], nd[kUnroll], du[kUnroll], dvv[kUnroll];
+              uint32_t* const q = team_q + (tid >> 5) * (5 * kTeamQ);
+              uint32_t* const qiu = q;               // improvement candidates: u
+              uint32_t* const qid = q + kTeamQ;      //   tentative distance
+              uint32_t* const qpu = q + 2 * kTeamQ;  // DAG predecessors: u
+              uint32_t* const qpv = q + 3 * kTeamQ;  //   v (row owner)
+              uint32_t* const qps = q + 4 * kTeamQ;  //   slot of v's row
+              uint32_t iq_n = 0, pq_n = 0;           // warp-uniform queue lengths
+              // Pass 2a: the last `m` improvement candidates, one per lane:
+              // atomicMin and min-weight gather in flight together; Delta
+              // candidates need no atomic result (a lane that lost the race
+              // recorded a key >= the winner's); queue appends ballot-aggregated.
+              auto drain_imp = [&](uint32_t m) {
+                const uint32_t i = iq_n - m + lane;
+                const bool act = lane < m;
+                uint32_t u = 0, nd = 0, old = kInfDist, mw = 0;
+                if (act) {
+                  u = qiu[i];
+                  nd = qid[i];
+                  old = dist.fetch_min(u, nd);
+                  if (nd < Fu) mw = __ldg(g.minw + u);
+                }
+                if (act && nd < Fu) kmin = min(kmin, nd + mw);
+                const bool imp = act && nd < old;
+                c_impr += imp;
+                const uint32_t bn = __ballot_sync(0xffffffffu, imp && nd < Fu && old >= Fu);
+                const uint32_t bf = __ballot_sync(0xffffffffu, imp && nd >= Fu && old == kInfDist);
+                if (bn | bf) {
+                  uint32_t b_n = 0, b_f = 0;
+                  if (lane == 0) {
+                    if (bn) b_n = atomicAdd(&R.near_app, __popc(bn));
+                    if (bf) b_f = atomicAdd(&R.far_app, __popc(bf));
+                  }
+                  b_n = near_len + __shfl_sync(0xffffffffu, b_n, 0);
+                  b_f = far_len + __shfl_sync(0xffffffffu, b_f, 0);
+                  if (bn >> lane & 1u) nqc[b_n + __popc(bn & lt)] = u;
+                  if (bf >> lane & 1u) fqc[b_f + __popc(bf & lt)] = u;
+                }
+                iq_n -= m;
+              };
+              // Pass 2b: the last `m` DAG predecessors: sigma pull (fp64 RED,
+              // integer-valued so exact in any order) and the DAG record.
+              auto drain_pred = [&](uint32_t m) {
+                const uint32_t i = pq_n - m + lane;
+                const bool act = lane < m;
+                uint32_t v = 0, sl = 0;
+                double sg = 0.0;
+                if (act) {
+                  const uint32_t u = qpu[i];
+                  v = qpv[i];
+                  sl = qps[i];
+                  sg = __ldcg(sigma + u);
+                }
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&R.dag_app, m);
+                base = dag_len + __shfl_sync(0xffffffffu, base, 0);
+                if (act) {
+                  atomicAdd(sigma + v, sg);
+                  if (base + lane < dag_cap)
+                    dag[base + lane] = make_uint2(sl, v);
+                  else
+                    over = true;
+                }
+                pq_n -= m;
+              };
+              // Pass 1: stream kUnroll groups of 32 edges; software-pipelined:
+              // the next step's slot words are in flight while this step's
+              // distance gathers resolve.  Only lanes that need more work are
+              // kept (compacted into the warp's queues).
+              // Slot words stay packed until used (PACKED: one register).
+              using Word = typename std::conditional<PACKED, uint32_t, uint2>::type;
+              constexpr Word kNoWord = Word{};
+              int jj[kUnroll];
+              Word xw[kUnroll];
+              auto fetch = [&](uint32_t e0) {
+                uint32_t slot[kUnroll];
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
                   const uint32_t eg = e0 + 32 * k;
@@ -252,84 +347,73 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
                   const uint32_t e = eg + lane;
                   slot[k] = e < we ? sh.rowadj[jj[k]] + e : 0xFFFFFFFFu;
                 }
-                // B, C: slot stream, then the distance gathers
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
-                  uint32_t w = 0;
-                  uu[k] = 0;
-                  if (slot[k] != 0xFFFFFFFFu) load_slot<PACKED>(g, slot[k], uu[k], w, stream_pol);
-                  dvv[k] = sh.dv[jj[k]];
-                  nd[k] = dvv[k] + w;
-                }
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) du[k] = slot[k] != 0xFFFFFFFFu ? dist.load(uu[k]) : 0u;
-                // D: every dependent access of the kUnroll groups in flight at once
-                bool pr[kUnroll], im[kUnroll];
-                uint32_t old[kUnroll], mw[kUnroll];
-                double sg[kUnroll];
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
-                  const bool valid = slot[k] != 0xFFFFFFFFu;
-                  // u precedes v on a shortest path: d[u] + w == d[v]  (nd - dv == w)
-                  pr[k] = valid && du[k] != kInfDist && du[k] + (nd[k] - dvv[k]) == dvv[k];
-                  im[k] = valid && nd[k] < du[k];
-                }
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) old[k] = im[k] ? dist.fetch_min(uu[k], nd[k]) : kInfDist;
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) mw[k] = (im[k] && nd[k] < Fu) ? __ldg(g.minw + uu[k]) : 0u;
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) sg[k] = pr[k] ? __ldcg(sigma + uu[k]) : 0.0;
-                // E: consume.  Delta candidates need no atomic result: a lane
-                // that lost the race recorded a key >= the winner's.
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k)
-                  if (im[k] && nd[k] < Fu) kmin = min(kmin, nd[k] + mw[k]);
-                // sigma pull: fire-and-forget fp64 RED (integer-valued: exact in any order)
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k)
-                  if (pr[k]) atomicAdd(sigma + sh.v[jj[k]], sg[k]);
-                // appends: one ballot-aggregated atomic per queue per warp iteration
-                uint32_t bd[kUnroll], bn[kUnroll], bf[kUnroll];
-                uint32_t cd = 0, cn = 0, cf = 0;
-#pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
-                  const bool imp = im[k] && nd[k] < old[k];
-                  c_impr += imp;
-                  bd[k] = __ballot_sync(0xffffffffu, pr[k]);
-                  bn[k] = __ballot_sync(0xffffffffu, imp && nd[k] < Fu && old[k] >= Fu);
-                  bf[k] = __ballot_sync(0xffffffffu, imp && nd[k] >= Fu && old[k] == kInfDist);
-                  cd += __popc(bd[k]);
-                  cn += __popc(bn[k]);
-                  cf += __popc(bf[k]);
-                }
-                if (cd | cn | cf) {
-                  uint32_t base_d = 0, base_n = 0, base_f = 0;
-                  if (lane == 0) {
-                    if (cd) base_d = atomicAdd(&R.dag_app, cd);
-                    if (cn) base_n = atomicAdd(&R.near_app, cn);
-                    if (cf) base_f = atomicAdd(&R.far_app, cf);
+                  xw[k] = kNoWord;
+                  if (slot[k] != 0xFFFFFFFFu) {
+                    if constexpr (PACKED)
+                      xw[k] = ld_stream_u32(g.slots32 + slot[k], stream_pol);
+                    else
+                      xw[k] = ld_stream_u64(g.slots64 + slot[k], stream_pol);
                   }
-                  base_d = dag_len + __shfl_sync(0xffffffffu, base_d, 0);
-                  base_n = near_len + __shfl_sync(0xffffffffu, base_n, 0);
-                  base_f = far_len + __shfl_sync(0xffffffffu, base_f, 0);
+                }
+              };
+              auto nbr = [&](const Word& x) -> uint32_t {
+                if constexpr (PACKED) return x >> g.wbits; else return x.x;
+              };
+              auto wgt = [&](const Word& x) -> uint32_t {
+                if constexpr (PACKED) return x & g.wmask; else return x.y;
+              };
+              fetch(wb);
+              for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
+                uint32_t du[kUnroll];
+                Word cx[kUnroll];
+                int cj[kUnroll];
 #pragma unroll
-                  for (int k = 0; k < kUnroll; ++k) {
-                    if (bd[k] >> lane & 1u) {
-                      const uint32_t pos = base_d + __popc(bd[k] & lt);
-                      if (pos < dag_cap)
-                        dag[pos] = make_uint2(slot[k], sh.v[jj[k]]);
-                      else
-                        over = true;
-                    }
-                    if (bn[k] >> lane & 1u) nq[nc][base_n + __popc(bn[k] & lt)] = uu[k];
-                    if (bf[k] >> lane & 1u) fq[fc][base_f + __popc(bf[k] & lt)] = uu[k];
-                    base_d += __popc(bd[k]);
-                    base_n += __popc(bn[k]);
-                    base_f += __popc(bf[k]);
+                for (int k = 0; k < kUnroll; ++k) {
+                  const bool valid = e0 + 32 * k + lane < we;
+                  du[k] = valid ? dist.load(nbr(xw[k])) : 0u;
+                  cx[k] = xw[k];
+                  cj[k] = jj[k];
+                }
+                if (e0 + 32 * kUnroll < we) fetch(e0 + 32 * kUnroll);
+#pragma unroll
+                for (int k = 0; k < kUnroll; ++k) {
+                  const uint32_t e = e0 + 32 * k + lane;
+                  const bool valid = e < we;
+                  const uint32_t dv = sh.dv[cj[k]];
+                  const uint32_t u = nbr(cx[k]), w = wgt(cx[k]);
+                  const uint32_t nd = dv + w;
+                  // u precedes v on a shortest path (d[u] + w == d[v]); u then
+                  // settled in an earlier round, so sigma[u] is final
+                  const bool isp = valid && du[k] != kInfDist && du[k] + w == dv;
+                  const bool isi = valid && nd < du[k];
+                  const uint32_t bp = __ballot_sync(0xffffffffu, isp);
+                  const uint32_t bi = __ballot_sync(0xffffffffu, isi);
+                  if (isi) {
+                    const uint32_t pos = iq_n + __popc(bi & lt);
+                    qiu[pos] = u;
+                    qid[pos] = nd;
                   }
+                  if (isp) {
+                    const uint32_t pos = pq_n + __popc(bp & lt);
+                    qpu[pos] = u;
+                    qpv[pos] = sh.v[cj[k]];
+                    qps[pos] = sh.rowadj[cj[k]] + e;
+                  }
+                  iq_n += __popc(bi);
+                  pq_n += __popc(bp);
+                }
+                if (iq_n >= 32 || pq_n >= 32) {
+                  __syncwarp();
+                  while (iq_n >= 32) drain_imp(32);
+                  while (pq_n >= 32) drain_pred(32);
+                  __syncwarp();
                 }
               }
+              __syncwarp();
+              if (iq_n) drain_imp(iq_n);
+              if (pq_n) drain_pred(pq_n);
             }
             __syncthreads();  // staged chunk fully consumed
             j += cnt;
@@ -367,14 +451,15 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         uint32_t lkey = kInfDist, lfar = kInfDist;
         c_far += (rank == 0) ? far_len : 0;
         c_refill += (rank == 0) ? 1 : 0;
-        const uint32_t* src = fq[fc];
-        uint32_t* dst = fq[fc ^ 1];
+        const uint32_t* src = fc ? fq1 : fq0;
+        uint32_t* dst = fc ? fq0 : fq1;
+        uint32_t* const nqc = nc ? nq1 : nq0;
         for (uint32_t i = gtid; i < far_len; i += TT) {
           const uint32_t u = __ldcg(src + i);
           const uint32_t du = dist.load(u);
           if (du >= Fo) {  // du < Fo: already near or settled
             if (du < Fn) {
-              nq[nc][near_len + team_append(&R.near_app)] = u;
+              nqc[near_len + team_append(&R.near_app)] = u;
               lkey = min(lkey, du + __ldg(g.minw + u));
             } else {
               dst[team_append(&R.far_app)] = u;
@@ -404,8 +489,8 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         TeamRed& R = cur();
         uint32_t lkept = kInfDist;
         c_near += (rank == 0) ? near_len : 0;
-        const uint32_t* src = nq[nc];
-        uint32_t* dst = nq[nc ^ 1];
+        const uint32_t* src = nc ? nq1 : nq0;
+        uint32_t* dst = nc ? nq0 : nq1;
         const uint32_t sb = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * rank) / C);
         const uint32_t se = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * (rank + 1)) / C);
         // warp-level: each warp scans 32 entries, one packed atomic hands out

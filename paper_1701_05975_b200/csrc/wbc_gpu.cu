@@ -199,6 +199,7 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
               : g->tune_cluster <= 8 ? 8 : 16;
     s.threads = 1024;
+    s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
   }
   // Skewed graphs run on the team kernel (bc_team.cuh).  One CTA per source
@@ -209,6 +210,7 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   if (g->tune_cluster < 0 && !tiny && g->hot_coverage_25k >= 0.4) {
     s.cluster = n * 4 * static_cast<uint64_t>(g->sm_count) <= (64ULL << 20) ? 1 : 2;
     s.threads = 1024;
+    s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
   }
   if (g->tune_threads)
@@ -254,6 +256,8 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
       const void* f = reinterpret_cast<const void*>(pick_team(shape.cluster, g->packed, prof));
       if (shape.cluster > 8)
         WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(shape.dyn_smem)));
     }
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
@@ -263,6 +267,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(shape.cluster * g->sm_count, 1, 1);
     cfg.blockDim = dim3(shape.threads, 1, 1);
+    cfg.dynamicSmemBytes = shape.dyn_smem;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
@@ -392,7 +397,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(slots * shape.cluster, 1, 1);
     cfg.blockDim = dim3(shape.threads, 1, 1);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = shape.dyn_smem;
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
