@@ -99,7 +99,7 @@ def load_traffic(workload: str):
     with open(p) as f:
         d = json.load(f)
     e = d.get(workload)
-    return None if e is None else float(e["dram_bytes_per_source"])
+    return None if e is None else (float(e["dram_bytes_per_source"]), e.get("kernel"))
 
 
 class ClockSampler:
@@ -373,10 +373,13 @@ def main():
         avg_launch = sum(kernel_s) / len(kernel_s)
         achieved = per_launch_bytes / avg_launch / 1e9
         tps = load_traffic(args.workload)
+        kname = gg.last_kernel()
+        # ncu traffic is only quoted for the kernel variant it was captured on
+        traffic = tps[0] * len(shard) if tps is not None and tps[1] == kname else None
         roofline = dict(bound="hbm", achieved=round(achieved, 1), peak=peak, unit="GB/s",
                         frac=round(achieved / peak, 4),
-                        traffic=None if tps is None else tps * len(shard),
-                        peak_source=peak_src, kernel="bc_sources_kernel",
+                        traffic=traffic, traffic_unit="bytes per launch (ncu dram read+write)",
+                        peak_source=peak_src, kernel=gg.last_kernel(),
                         bytes_model="72m+88n per source (SURVEY.md 8d)",
                         launch_ms=round(avg_launch * 1e3, 3))
         line = dict(metric=METRIC, value=round(value, 3), unit="GTEPS", n_gpus=world, steps=args.steps,

@@ -95,6 +95,10 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
  * boundaries (level L = order[level_ends[L], level_ends[L+1])),
  * *levels = depth.  Within a level the GPU's order is unspecified; compare
  * levels as sets. */
+/* The kernel the last run launched, e.g. "bc_team_kernel<1024,2>"
+ * (NUL-terminated, truncated to cap bytes). */
+int wbc_gpu_last_kernel(wbc_gpu_graph* g, char* buf, size_t cap);
+
 /* Test introspection: the shortest-path DAG edges one source recorded, per
  * level (pred[i] -> succ[i] in caller ids; level L's edges are
  * [dag_ends[L], dag_ends[L+1])).  pred/succ need room for 2m entries,

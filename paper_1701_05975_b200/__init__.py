@@ -390,6 +390,11 @@ class GpuGraph:
         L.load().wbc_gpu_last_run_stats(self._h, _p(st))
         return dict(slots=int(st[0]), threads=int(st[1]), dag_overflow_sources=int(st[2]), launches=int(st[3]))
 
+    def last_kernel(self) -> str:
+        buf = C.create_string_buffer(96)
+        L.load().wbc_gpu_last_kernel(self._h, buf, len(buf))
+        return buf.value.decode()
+
     def bc(self, opt: Optional[EngineOptions] = None) -> BcResult:
         """bc_parallel semantics on the resident graph (engine.cpp:372-457)."""
         opt = opt or EngineOptions()

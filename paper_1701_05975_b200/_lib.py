@@ -32,6 +32,7 @@ SIGNATURES = [
     ("wbc_gpu_bc", i32, [vp, vp, u64, u32, vp, vp, vp, C.POINTER(f64)]),
     ("wbc_gpu_bc_device", i32, [vp, vp, u64, u32, vp, vp, vp, vp]),
     ("wbc_gpu_sssp_dump", i32, [vp, u32, vp, vp, vp, C.POINTER(u32)]),
+    ("wbc_gpu_last_kernel", i32, [vp, C.c_char_p, C.c_size_t]),
     ("wbc_gpu_sssp_dag", i32, [vp, u32, vp, vp, vp, C.POINTER(u32), C.POINTER(u32)]),
     ("wbc_gpu_sssp_levels", i32, [vp, u32, vp, C.POINTER(u32), vp, C.POINTER(u32)]),
     ("wbc_gpu_graph_info", i32, [vp, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32), C.POINTER(i32),

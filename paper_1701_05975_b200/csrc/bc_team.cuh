@@ -493,52 +493,86 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         uint32_t* dst = nc ? nq0 : nq1;
         const uint32_t sb = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * rank) / C);
         const uint32_t se = static_cast<uint32_t>((static_cast<uint64_t>(near_len) * (rank + 1)) / C);
-        // warp-level: each warp scans 32 entries, one packed atomic hands out
-        // (order position, edge offset) for its settled lanes; no CTA barrier
+        // warp-level, kSettleU entries per lane per step: the near-queue
+        // loads, distance and row-offset gathers of the step are in flight
+        // together; a warp scan plus one packed atomic hands out (order
+        // position, edge offset) for the settled lanes; no CTA barrier.
+        constexpr int kSettleU = 4;
         const uint32_t lane = tid & 31;
-        for (uint32_t c = sb + (tid & ~31u); c < se; c += T) {
-          const uint32_t i = c + lane;
-          uint32_t u = 0, du = kInfDist, row = 0, deg = 0;
-          const bool have = i < se;
-          if (have) {
-            u = __ldcg(src + i);
-            du = dist.load(u);
+        const uint32_t lt = (1u << lane) - 1u;
+        for (uint32_t c = sb + (tid & ~31u) * kSettleU; c < se; c += T * kSettleU) {
+          uint32_t u[kSettleU], du[kSettleU], row[kSettleU], deg[kSettleU];
+          bool have[kSettleU], st[kSettleU];
+#pragma unroll
+          for (int k = 0; k < kSettleU; ++k) {
+            const uint32_t i = c + 32 * k + lane;
+            have[k] = i < se;
+            u[k] = have[k] ? __ldcg(src + i) : 0u;
           }
-          const bool st = have && du < thr;
-          if (st) {
-            row = __ldg(g.offsets + u);
-            deg = __ldg(g.offsets + u + 1) - row;
+#pragma unroll
+          for (int k = 0; k < kSettleU; ++k) du[k] = have[k] ? dist.load(u[k]) : kInfDist;
+#pragma unroll
+          for (int k = 0; k < kSettleU; ++k) {
+            st[k] = have[k] && du[k] < thr;
+            row[k] = st[k] ? __ldg(g.offsets + u[k]) : 0u;
+            deg[k] = st[k] ? __ldg(g.offsets + u[k] + 1) : 0u;
           }
-          const uint32_t bs = __ballot_sync(0xffffffffu, st);
-          if (bs) {
-            uint32_t pe = deg;  // inclusive warp scan of degrees
+          uint32_t bs[kSettleU], pe[kSettleU], nset = 0, eset = 0;
+#pragma unroll
+          for (int k = 0; k < kSettleU; ++k) {
+            deg[k] -= row[k];
+            bs[k] = __ballot_sync(0xffffffffu, st[k]);
+            pe[k] = deg[k];  // inclusive warp scan of degrees
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, pe, o);
-              if (lane >= static_cast<uint32_t>(o)) pe += y;
+              const uint32_t y = __shfl_up_sync(0xffffffffu, pe[k], o);
+              if (lane >= static_cast<uint32_t>(o)) pe[k] += y;
             }
-            const uint32_t wtot = __shfl_sync(0xffffffffu, pe, 31);
+            // exclusive prefix of this lane within the whole step
+            pe[k] = pe[k] - deg[k] + eset;
+            eset += __shfl_sync(0xffffffffu, pe[k] + deg[k], 31) - eset;
+            nset += __popc(bs[k]);
+          }
+          if (nset) {
             unsigned long long base = 0;
-            if (lane == 0) base = atomicAdd(&R.ord, (static_cast<unsigned long long>(__popc(bs)) << 32) | wtot);
+            if (lane == 0) base = atomicAdd(&R.ord, (static_cast<unsigned long long>(nset) << 32) | eset);
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (st) {
-              const uint32_t pos = ord_len + static_cast<uint32_t>(base >> 32) + __popc(bs & ((1u << lane) - 1u));
-              order[pos] = u;
-              ord_d[pos] = du;
-              ord_row[pos] = row;
-              epref[pos] = ord_edges + static_cast<uint32_t>(base) + (pe - deg);
-              sigma[u] = 0.0;
-              delta[u] = 0.0;
+            uint32_t pos = ord_len + static_cast<uint32_t>(base >> 32);
+            const uint32_t ebase = ord_edges + static_cast<uint32_t>(base);
+#pragma unroll
+            for (int k = 0; k < kSettleU; ++k) {
+              if (st[k]) {
+                const uint32_t q = pos + __popc(bs[k] & lt);
+                order[q] = u[k];
+                ord_d[q] = du[k];
+                ord_row[q] = row[k];
+                epref[q] = ebase + pe[k];
+                sigma[u[k]] = 0.0;
+                delta[u[k]] = 0.0;
+              }
+              pos += __popc(bs[k]);
             }
           }
-          const uint32_t bk = __ballot_sync(0xffffffffu, have && !st);
-          if (bk) {
+          uint32_t bk[kSettleU], nkeep = 0;
+#pragma unroll
+          for (int k = 0; k < kSettleU; ++k) {
+            bk[k] = __ballot_sync(0xffffffffu, have[k] && !st[k]);
+            nkeep += __popc(bk[k]);
+          }
+          if (nkeep) {
             uint32_t kb = 0;
-            if (lane == 0) kb = atomicAdd(&R.keep_app, __popc(bk));
+            if (lane == 0) kb = atomicAdd(&R.keep_app, nkeep);
             kb = __shfl_sync(0xffffffffu, kb, 0);
-            if (have && !st) {
-              dst[kb + __popc(bk & ((1u << lane) - 1u))] = u;
-              lkept = min(lkept, du + __ldg(g.minw + u));
+            uint32_t mw[kSettleU];
+#pragma unroll
+            for (int k = 0; k < kSettleU; ++k) mw[k] = (bk[k] >> lane & 1u) ? __ldg(g.minw + u[k]) : 0u;
+#pragma unroll
+            for (int k = 0; k < kSettleU; ++k) {
+              if (bk[k] >> lane & 1u) {
+                dst[kb + __popc(bk[k] & lt)] = u[k];
+                lkept = min(lkept, du[k] + mw[k]);
+              }
+              kb += __popc(bk[k]);
             }
           }
         }

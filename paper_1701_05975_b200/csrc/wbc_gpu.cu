@@ -126,6 +126,7 @@ struct wbc_gpu_graph {
   bool ws_team = false;        // workspace carries the team-kernel arrays
   bool profiling = false;
   uint64_t stats[4] = {0, 0, 0, 0};
+  std::string last_kernel;
   uint64_t prof_host[wbc_dev::kProfCounters] = {};
 
   ~wbc_gpu_graph() {
@@ -410,6 +411,9 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
   g->stats[1] = shape.threads * std::max(1, shape.cluster);
+  g->last_kernel = shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
+                                           std::to_string(shape.cluster) + ">"
+                                     : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
   g->stats[3] = 2;
   return WBC_OK;
 }
@@ -782,6 +786,14 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
   cudaFree(d_src);
   cudaFree(d_dep);
   return rc;
+}
+
+int wbc_gpu_last_kernel(wbc_gpu_graph* g, char* buf, size_t cap) {
+  if (!g || !buf || !cap) return set_error(WBC_E_INVALID, "null argument");
+  const size_t k = std::min(cap - 1, g->last_kernel.size());
+  std::memcpy(buf, g->last_kernel.data(), k);
+  buf[k] = 0;
+  return WBC_OK;
 }
 
 int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t* succ,

@@ -20,7 +20,7 @@ def declared_functions():
 
 def test_header_declares_the_boundary():
     names = declared_functions()
-    for must in ("wbc_gpu_graph_create", "wbc_gpu_bc", "wbc_gpu_sssp_dump", "wbc_gpu_sssp_levels", "wbc_gpu_sssp_dag", "wbc_gpu_graph_destroy",
+    for must in ("wbc_gpu_graph_create", "wbc_gpu_bc", "wbc_gpu_sssp_dump", "wbc_gpu_sssp_levels", "wbc_gpu_sssp_dag", "wbc_gpu_last_kernel", "wbc_gpu_graph_destroy",
                  "wbc_gpu_last_error", "wbc_gpu_bc_device"):
         assert must in names
 

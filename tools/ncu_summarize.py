@@ -1,4 +1,4 @@
-"""Summarise an ncu --set full report of bc_sources_kernel into markdown.
+"""Summarise an ncu --set full report of BC kernel (bc_team_kernel / bc_sources_kernel) into markdown.
 
     python tools/ncu_summarize.py gpurun_out/prof.ncu-rep --sources 296 > profiles/rNN_x.md
 """
