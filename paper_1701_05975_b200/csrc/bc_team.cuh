@@ -56,13 +56,19 @@ __device__ __forceinline__ void team_red_reset(TeamRed& r) {
   r.flags = 0;
 }
 
+// Frontier vertices staged per chunk: at least 128, so a one-warp team
+// relaxes a typical large-diameter level (~50 vertices) in one chunk.
+template <int T>
+constexpr int team_chunk() { return T < 128 ? 128 : T; }
+
 template <int T>
 struct TeamShared {
-  uint32_t v[T];
-  uint32_t dv[T];
-  uint32_t rowadj[T];  // row start + chunk base - first edge (mod 2^32)
-  uint32_t pref[T + 1];
-  double acc[T];
+  static constexpr int CH = team_chunk<T>();
+  uint32_t v[CH];
+  uint32_t dv[CH];
+  uint32_t rowadj[CH];  // row start + chunk base - first edge (mod 2^32)
+  uint32_t pref[CH + 1];
+  double acc[CH];
   TeamRed ring[4];     // used through rank 0's copy
   uint32_t bcast;
 };
@@ -117,8 +123,12 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
 constexpr uint32_t kTeamQ = 32 * kUnroll + 32;
 __host__ __device__ constexpr size_t team_dyn_smem(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
 
+// 1024-thread CTAs: one per SM.  32-thread CTAs (one warp per source, for
+// large-diameter graphs whose rounds are latency-bound): 16 per SM, 128 regs.
+constexpr int team_min_blocks(int threads) { return threads >= 1024 ? 1 : (threads >= 128 ? 2048 / threads : 16); }
+
 template <int T, int C, bool PACKED, bool PROF>
-__global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
+__global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const RunParams p) {
   __shared__ TeamShared<T> sh;
   extern __shared__ uint32_t team_q[];
   const GraphView& g = p.g;
@@ -186,22 +196,38 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
   // Stages the edges [cb, my_e) of the level's vertices starting at order
   // position j (edge prefix epref, vertices j.. have epref < my_e) into
   // shared memory; returns the chunk's vertex count and sets ce.
+  constexpr int CH = TeamShared<T>::CH;
   auto stage = [&](uint32_t j, uint32_t fe, uint32_t cb, uint32_t my_e, uint32_t Ee, uint32_t& ce) -> int {
-    const uint32_t jt = j + tid;
-    uint32_t gs = Ee;
-    if (jt < fe) gs = __ldcg(epref + jt);
-    const bool use = jt < fe && gs < my_e;
-    if (use) {
-      sh.v[tid] = __ldcg(order + jt);
-      sh.dv[tid] = __ldcg(ord_d + jt);
-      sh.rowadj[tid] = __ldcg(ord_row + jt) + cb - gs;
-      sh.pref[tid] = (gs > cb ? gs : cb) - cb;
-      sh.acc[tid] = 0.0;
+    constexpr int R = CH / T;
+    uint32_t gs[R], ov[R], od[R], orow[R];
+    bool use[R];
+    // every load of the chunk in flight before the first barrier
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t jt = j + r * T + tid;
+      gs[r] = jt < fe ? __ldcg(epref + jt) : Ee;
+      ov[r] = jt < fe ? __ldcg(order + jt) : 0u;
+      od[r] = jt < fe ? __ldcg(ord_d + jt) : 0u;
+      orow[r] = jt < fe ? __ldcg(ord_row + jt) : 0u;
     }
-    if (tid == T - 1) sh.bcast = (j + T < fe) ? __ldcg(epref + j + T) : Ee;
-    const int cnt = __syncthreads_count(use);
-    const uint32_t nxt = sh.bcast;
-    ce = (cnt < T) ? my_e : min(nxt, my_e);
+    const uint32_t nxt = (tid == T - 1 && j + CH < fe) ? __ldcg(epref + j + CH) : Ee;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t t = r * T + tid;
+      use[r] = j + t < fe && gs[r] < my_e;
+      if (use[r]) {
+        sh.v[t] = ov[r];
+        sh.dv[t] = od[r];
+        sh.rowadj[t] = orow[r] + cb - gs[r];
+        sh.pref[t] = (gs[r] > cb ? gs[r] : cb) - cb;
+        sh.acc[t] = 0.0;
+      }
+    }
+    if (tid == T - 1) sh.bcast = nxt;
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) cnt += __syncthreads_count(use[r]);
+    ce = (cnt < CH) ? my_e : min(sh.bcast, my_e);
     if (tid == 0) sh.pref[cnt] = ce - cb;
     __syncthreads();
     return cnt;
@@ -254,7 +280,7 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         const uint32_t my_e = Eb + static_cast<uint32_t>((static_cast<uint64_t>(E) * (rank + 1)) / C);
         c_relax += (rank == 0) ? E : 0;
         if (my_b < my_e) {
-          uint32_t j = block_find<T>(epref, fb, fe, my_b);
+          uint32_t j = C == 1 ? fb : block_find<T>(epref, fb, fe, my_b);
           uint32_t cb = my_b;
           while (cb < my_e) {
             uint32_t ce;
@@ -454,16 +480,26 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         const uint32_t* src = fc ? fq1 : fq0;
         uint32_t* dst = fc ? fq0 : fq1;
         uint32_t* const nqc = nc ? nq1 : nq0;
-        for (uint32_t i = gtid; i < far_len; i += TT) {
-          const uint32_t u = __ldcg(src + i);
-          const uint32_t du = dist.load(u);
-          if (du >= Fo) {  // du < Fo: already near or settled
-            if (du < Fn) {
-              nqc[near_len + team_append(&R.near_app)] = u;
-              lkey = min(lkey, du + __ldg(g.minw + u));
-            } else {
-              dst[team_append(&R.far_app)] = u;
-              lfar = min(lfar, du);
+        constexpr int kRefillU = T <= 32 ? 8 : 4;  // far entries per lane per step
+        for (uint32_t c = gtid; c < far_len; c += TT * kRefillU) {
+          uint32_t u[kRefillU], du[kRefillU];
+#pragma unroll
+          for (int k = 0; k < kRefillU; ++k) {
+            const uint32_t i = c + k * TT;
+            u[k] = i < far_len ? __ldcg(src + i) : 0u;
+          }
+#pragma unroll
+          for (int k = 0; k < kRefillU; ++k) du[k] = c + k * TT < far_len ? dist.load(u[k]) : 0u;
+#pragma unroll
+          for (int k = 0; k < kRefillU; ++k) {
+            if (c + k * TT < far_len && du[k] >= Fo) {  // du < Fo: already near or settled
+              if (du[k] < Fn) {
+                nqc[near_len + team_append(&R.near_app)] = u[k];
+                lkey = min(lkey, du[k] + __ldg(g.minw + u[k]));
+              } else {
+                dst[team_append(&R.far_app)] = u[k];
+                lfar = min(lfar, du[k]);
+              }
             }
           }
         }
@@ -497,7 +533,7 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         // loads, distance and row-offset gathers of the step are in flight
         // together; a warp scan plus one packed atomic hands out (order
         // position, edge offset) for the settled lanes; no CTA barrier.
-        constexpr int kSettleU = 4;
+        constexpr int kSettleU = T <= 32 ? 8 : 4;
         const uint32_t lane = tid & 31;
         const uint32_t lt = (1u << lane) - 1u;
         for (uint32_t c = sb + (tid & ~31u) * kSettleU; c < se; c += T * kSettleU) {
@@ -601,15 +637,27 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
       for (uint32_t L = nlev - 1; L >= 1; --L) {
         // dag_ends[nlev] is written by the leader in this very phase: use the register
         const uint32_t b = __ldcg(dag_ends + L), e = L + 1 == nlev ? dag_len : __ldcg(dag_ends + L + 1);
-        for (uint32_t i = b + gtid; i < e; i += TT) {
-          const uint2 d = __ldcg(dag + i);
-          uint32_t u, w;
-          load_slot<PACKED>(g, d.x, u, w);
-          const uint32_t v = d.y;
-          // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
-          const double c = __ldcg(sigma + u) / __ldcg(sigma + v) * (1.0 + __ldcg(delta + v));
-          atomicAdd(delta + u, c);
-          if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + d.x), c);
+        constexpr int kBackU = 4;  // DAG edges per thread per step, loads in flight together
+        for (uint32_t c = b + gtid; c < e; c += TT * kBackU) {
+          uint2 d[kBackU];
+          uint32_t u[kBackU];
+#pragma unroll
+          for (int k = 0; k < kBackU; ++k) d[k] = c + k * TT < e ? __ldcg(dag + c + k * TT) : make_uint2(0, 0);
+#pragma unroll
+          for (int k = 0; k < kBackU; ++k) {
+            uint32_t w;
+            u[k] = 0;
+            if (c + k * TT < e) load_slot<PACKED>(g, d[k].x, u[k], w);
+          }
+#pragma unroll
+          for (int k = 0; k < kBackU; ++k) {
+            if (c + k * TT >= e) continue;
+            const uint32_t v = d[k].y;
+            // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
+            const double cc = __ldcg(sigma + u[k]) / __ldcg(sigma + v) * (1.0 + __ldcg(delta + v));
+            atomicAdd(delta + u[k], cc);
+            if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + d[k].x), cc);
+          }
         }
         // level L's delta is final (levels > L were done in earlier phases)
         const uint32_t vb = __ldcg(lev + L), ve = L + 1 == nlev ? ord_len : __ldcg(lev + L + 1);
@@ -632,7 +680,7 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
         const uint32_t my_b = lEb + static_cast<uint32_t>((static_cast<uint64_t>(E) * rank) / C);
         const uint32_t my_e = lEb + static_cast<uint32_t>((static_cast<uint64_t>(E) * (rank + 1)) / C);
         if (my_b < my_e) {
-          uint32_t j = block_find<T>(epref, pb, pe, my_b);
+          uint32_t j = C == 1 ? pb : block_find<T>(epref, pb, pe, my_b);
           uint32_t cb = my_b;
           while (cb < my_e) {
             uint32_t ce;
@@ -650,7 +698,8 @@ __global__ void __launch_bounds__(T, 1) bc_team_kernel(const RunParams p) {
               }
             });
             __syncthreads();
-            if (tid < cnt && sh.acc[tid] != 0.0) atomicAdd(delta + sh.v[tid], sh.acc[tid]);
+            for (int t = tid; t < cnt; t += T)
+              if (sh.acc[t] != 0.0) atomicAdd(delta + sh.v[t], sh.acc[t]);
             __syncthreads();
             j += cnt;
             cb = ce;

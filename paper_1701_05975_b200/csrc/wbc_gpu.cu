@@ -158,8 +158,9 @@ KernelFn pick_kernel(int threads, bool packed, bool prof = false) {
 }
 
 template <bool PACKED, bool PROF>
-KernelFn pick_team_t(int c) {
+KernelFn pick_team_t(int c, int threads) {
   using namespace wbc_dev;
+  if (threads <= 32) return bc_team_kernel<32, 1, PACKED, PROF>;
   switch (c) {
     case 1: return bc_team_kernel<1024, 1, PACKED, PROF>;
     case 2: return bc_team_kernel<1024, 2, PACKED, PROF>;
@@ -169,9 +170,9 @@ KernelFn pick_team_t(int c) {
   }
 }
 
-KernelFn pick_team(int c, bool packed, bool prof = false) {
-  if (packed) return prof ? pick_team_t<true, true>(c) : pick_team_t<true, false>(c);
-  return prof ? pick_team_t<false, true>(c) : pick_team_t<false, false>(c);
+KernelFn pick_team(int c, int threads, bool packed, bool prof = false) {
+  if (packed) return prof ? pick_team_t<true, true>(c, threads) : pick_team_t<true, false>(c, threads);
+  return prof ? pick_team_t<false, true>(c, threads) : pick_team_t<false, false>(c, threads);
 }
 
 struct LaunchShape {
@@ -199,7 +200,7 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   if (g->tune_cluster > 0) {
     s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
               : g->tune_cluster <= 8 ? 8 : 16;
-    s.threads = 1024;
+    s.threads = (s.cluster == 1 && g->tune_threads > 0 && g->tune_threads <= 32) ? 32 : 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
   }
@@ -220,6 +221,16 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.threads = 1024;
   else
     s.threads = 128;
+  // Flat, large graphs (grid / road-like: latency-bound rounds, small
+  // frontiers): one warp per source (grid-2048: 1.56 vs 1.1 GTEPS for the
+  // 128-thread per-CTA kernel).  Tiny graphs keep the per-CTA kernel with
+  // every distance in shared memory (ER-4096: 14.3 vs 11.8).
+  if (g->tune_cluster < 0 && !tiny && g->tune_threads == 0) {
+    s.cluster = 1;
+    s.threads = 32;
+    s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
+    return s;
+  }
   const void* fn = reinterpret_cast<const void*>(pick_kernel(s.threads, g->packed));
   cudaFuncAttributes attr{};
   cudaFuncGetAttributes(&attr, fn);
@@ -254,7 +265,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   int slots = 0;
   if (team) {
     for (const bool prof : {false, true}) {
-      const void* f = reinterpret_cast<const void*>(pick_team(shape.cluster, g->packed, prof));
+      const void* f = reinterpret_cast<const void*>(pick_team(shape.cluster, shape.threads, g->packed, prof));
       if (shape.cluster > 8)
         WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -272,8 +283,13 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int clusters = 0;
-    WBC_CUDA_TRY(cudaOccupancyMaxActiveClusters(
-        &clusters, reinterpret_cast<const void*>(pick_team(shape.cluster, g->packed)), &cfg));
+    const void* fk = reinterpret_cast<const void*>(pick_team(shape.cluster, shape.threads, g->packed));
+    if (shape.cluster == 1) {  // plain launch: resident CTAs per SM x SMs
+      WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&clusters, fk, shape.threads, shape.dyn_smem));
+      clusters *= g->sm_count;
+    } else {
+      WBC_CUDA_TRY(cudaOccupancyMaxActiveClusters(&clusters, fk, &cfg));
+    }
     if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
     slots = clusters;
   } else {
@@ -401,8 +417,8 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     cfg.dynamicSmemBytes = shape.dyn_smem;
     cfg.stream = stream;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(shape.cluster, g->packed, g->profiling), p));
+    cfg.numAttrs = shape.cluster > 1 ? 1 : 0;
+    WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(shape.cluster, shape.threads, g->packed, g->profiling), p));
   } else {
     pick_kernel(shape.threads, g->packed, g->profiling)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p);
     WBC_CUDA_TRY(cudaGetLastError());

@@ -15,12 +15,17 @@ from test_gpu_parity import assert_close, check_graph
 
 pytestmark = pytest.mark.gpu
 
-CLUSTERS = (1, 2, 4, 8, 16)
+# cluster size; "w" = one warp (32-thread CTA) per source
+CLUSTERS = (1, 2, 4, 8, 16, "w")
 
 
 def team_graph(W, g, c):
     gg = W.GpuGraph(g)
-    gg.set_param("cluster", c)
+    if c == "w":
+        gg.set_param("cluster", 1)
+        gg.set_param("threads", 32)
+    else:
+        gg.set_param("cluster", c)
     return gg
 
 
@@ -63,7 +68,7 @@ def test_team_race_and_dump(W, oracle, c):
 
 @pytest.mark.parametrize("c", CLUSTERS)
 def test_team_random_equivalence(W, oracle, c):
-    rng = np.random.default_rng(1234 + c)
+    rng = np.random.default_rng(1234 + (c if c != "w" else 99))
     for i in range(12):
         seed = int(rng.integers(1, 2**62))
         if i % 2 == 0:
@@ -90,7 +95,7 @@ def test_team_hub_rows_and_sampled(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8))
+@pytest.mark.parametrize("c", (1, 8, "w"))
 def test_team_dag_overflow_fallback(W, oracle, c):
     a = 60
     g = F.graph_of([(i, a + j, 1.0) for i in range(a) for j in range(a)])
@@ -100,7 +105,7 @@ def test_team_dag_overflow_fallback(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (2, 16))
+@pytest.mark.parametrize("c", (2, 16, "w"))
 def test_team_unpacked_slots(W, oracle, c):
     el = W.gen_er(3000, 6.0, 7)
     el.w = (np.random.default_rng(7).integers(1, 1_100_000, len(el))).astype(np.float64)
@@ -111,7 +116,7 @@ def test_team_unpacked_slots(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8))
+@pytest.mark.parametrize("c", (1, 8, "w"))
 def test_team_grid_large_diameter(W, oracle, c):
     el = W.assign_weights(W.gen_grid(64, 64), 1, 1000, 1)
     g = W.build_csr(el)
