@@ -382,7 +382,8 @@ class GpuGraph:
         if rc:
             _raise(rc)
         keys = ["rounds", "relaxed_slots", "near_scanned", "far_scanned", "refills", "improvements",
-                "dag_edges", "cyc_init", "cyc_relax", "cyc_threshold", "cyc_settle", "cyc_backward"]
+                "dag_edges", "cyc_init", "cyc_relax", "cyc_threshold", "cyc_settle", "cyc_backward",
+                "abort_near", "abort_front", "abort_dag", "abort_dist"]
         return {k: int(v) for k, v in zip(keys, out)}
 
     def last_run_stats(self) -> dict:

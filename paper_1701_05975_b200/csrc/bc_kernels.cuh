@@ -130,6 +130,7 @@ struct RunParams {
   uint32_t hot;            // device ids < hot keep their distance in shared memory
   uint32_t l2hot;          // device ids < l2hot get evict-last L2 hints
   unsigned long long* prof;  // null or kProfCounters per-run work counters
+  const unsigned long long* k_dev;  // if set, the source count is read here (device-side)
 };
 
 // Work counters (accumulated per source when RunParams::prof is set).
@@ -146,6 +147,10 @@ enum ProfCounter {
   kProfCyclesThreshold,
   kProfCyclesSettle,
   kProfCyclesBackward,
+  kProfAbortNear,   // bc_warp_kernel aborts, by cause
+  kProfAbortFront,
+  kProfAbortDag,
+  kProfAbortDist,
   kProfCounters
 };
 

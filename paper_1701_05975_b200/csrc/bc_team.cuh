@@ -233,10 +233,11 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
     return cnt;
   };
 
+  const unsigned long long k_total = p.k_dev ? __ldcg(p.k_dev) : p.k;
   for (;;) {
     tsync();
     const unsigned long long idx = prev().src;
-    if (idx >= p.k) break;
+    if (idx >= k_total) break;
     const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(idx);
     const uint32_t s = __ldg(p.inv + s_orig);
     if (timing) t_last = clock64();

@@ -25,6 +25,7 @@
 
 #include "bc_kernels.cuh"
 #include "bc_team.cuh"
+#include "bc_warp.cuh"
 #include "wbc_gpu.h"
 
 namespace {
@@ -106,7 +107,18 @@ struct wbc_gpu_graph {
   // workspace
   int ws_slots = 0;
   void* d_ws = nullptr;
+  uint64_t ws_bytes = 0;
   wbc_dev::Workspace ws{};
+  // warp-kernel layout of the same allocation, and the team-kernel layout
+  // its aborted sources are re-run on
+  wbc_dev::WarpParams wl{};
+  wbc_dev::Workspace ws_fb{};
+  int fb_slots = 0;
+  bool last_warp = false;     // the last run used bc_warp_kernel (layout wl / ws_fb)
+  uint32_t* d_abort_list = nullptr;
+  uint64_t abort_cap = 0;
+  unsigned long long* d_abort_count = nullptr;
+  unsigned long long* d_counter2 = nullptr;
   unsigned long long* d_counter = nullptr;
   unsigned int* d_overflow = nullptr;
   unsigned long long* d_prof = nullptr;
@@ -122,6 +134,7 @@ struct wbc_gpu_graph {
   int tune_slots = 0;
   int64_t tune_hot = -1;
   int64_t tune_l2hot = -1;
+  int tune_warp = 0;           // 1: bc_warp_kernel for flat graphs, 2: always (tests)
   int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
   bool ws_team = false;        // workspace carries the team-kernel arrays
   bool profiling = false;
@@ -133,6 +146,7 @@ struct wbc_gpu_graph {
     cudaSetDevice(device);
     for (void* p : {(void*)d_offsets, (void*)d_slots32, (void*)d_slots64, (void*)d_minw,
                     (void*)d_edge_id, (void*)d_perm, (void*)d_inv, d_ws, (void*)d_counter,
+                    (void*)d_abort_list, (void*)d_abort_count, (void*)d_counter2,
                     (void*)d_overflow, (void*)d_prof, (void*)d_node_dev, (void*)d_node,
                     (void*)d_edge, (void*)d_depth, (void*)d_sources})
       cudaFree(p);
@@ -176,6 +190,7 @@ KernelFn pick_team(int c, int threads, bool packed, bool prof = false) {
 }
 
 struct LaunchShape {
+  bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
   int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
   int threads = 128;
   uint32_t hot = 0;        // vertices with shared-memory distances
@@ -197,6 +212,14 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   LaunchShape s;
   const uint64_t n = g->n;
   const bool tiny = n * 4 <= 24 * 1024;
+  const bool warp_ok = true;  // distances >= 2^31-1 abort to the team kernel at run time
+  if (g->tune_warp == 2 && warp_ok) {  // forced (tests)
+    s.cluster = 1;
+    s.threads = 32;
+    s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
+    s.warp = true;
+    return s;
+  }
   if (g->tune_cluster > 0) {
     s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
               : g->tune_cluster <= 8 ? 8 : 16;
@@ -229,6 +252,10 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.cluster = 1;
     s.threads = 32;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
+    // the one-warp kernel with on-chip near set (bc_warp.cuh) is opt-in: it
+    // is instruction-latency-bound (~3K dependent warp instructions per
+    // round) and measured slower here (grid-2048: 1.03 vs 1.62 GTEPS)
+    s.warp = g->tune_warp != 0 && warp_ok;
     return s;
   }
   const void* fn = reinterpret_cast<const void*>(pick_kernel(s.threads, g->packed));
@@ -256,13 +283,104 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   return s;
 }
 
+// Per-slot workspace bytes of each kernel family.
+uint64_t ws_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, 64); }
+uint64_t ws_dcap(const wbc_gpu_graph* g, bool warp) {
+  const uint64_t n = g->n;
+  return warp ? round_up(n + n / 8 + 1024, 64) : round_up(n + n / 2 + 1024, 64);
+}
+uint64_t ws_per_slot(const wbc_gpu_graph* g, bool warp, bool team) {
+  const uint64_t ns = ws_ns(g);
+  if (warp) return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4) + ws_dcap(g, true) * 12;
+  return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? 20 : 0)) + ws_dcap(g, false) * 8;
+}
+
+wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slots, bool team) {
+  const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g, false);
+  auto carve = [&](uint64_t bytes) {
+    char* q = p;
+    p += bytes * slots;
+    return q;
+  };
+  wbc_dev::Workspace w{};
+  w.n_stride = ns;
+  w.dag_cap = dag_cap;
+  w.sigma = reinterpret_cast<double*>(carve(ns * 8));
+  w.delta = reinterpret_cast<double*>(carve(ns * 8));
+  w.dag = reinterpret_cast<uint2*>(carve(dag_cap * 8));
+  w.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.level_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.near_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  if (team) {
+    w.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.ord_row = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.epref = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.near_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.far_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  }
+  return w;
+}
+
+void carve_warp(wbc_gpu_graph* g, char* p, uint64_t slots) {
+  const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g, true);
+  auto carve = [&](uint64_t bytes) {
+    char* q = p;
+    p += bytes * slots;
+    return q;
+  };
+  wbc_dev::WarpParams& w = g->wl;
+  w.n_stride = ns;
+  w.dag_cap = dag_cap;
+  w.sigma = reinterpret_cast<double*>(carve(ns * 8));
+  w.delta = reinterpret_cast<double*>(carve(ns * 8));
+  w.dag = reinterpret_cast<uint2*>(carve(dag_cap * 8));
+  w.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.level_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.dag_slot = reinterpret_cast<uint32_t*>(carve(dag_cap * 4));
+}
+
+int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
+  if (g->d_ws && g->ws_bytes >= bytes) return WBC_OK;
+  cudaFree(g->d_ws);
+  g->d_ws = nullptr;
+  g->ws_bytes = 0;
+  void* base = nullptr;
+  const cudaError_t err = cudaMalloc(&base, bytes);
+  if (err != cudaSuccess)
+    return set_error(WBC_E_NOMEM, "workspace allocation of " + std::to_string(bytes) +
+                                      " bytes failed: " + cudaGetErrorString(err));
+  g->d_ws = base;
+  g->ws_bytes = bytes;
+  return WBC_OK;
+}
+
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
-  const uint64_t ns = round_up(uint64_t{g->n} + 2, 64);
-  const uint64_t dag_cap = round_up(uint64_t{g->n} + uint64_t{g->n} / 2 + 1024, 64);
   const bool team = shape.cluster > 0;
-  const uint64_t per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? 20 : 0)) + dag_cap * 8;
+  const uint64_t per_slot = ws_per_slot(g, shape.warp, team);
   int slots = 0;
+  if (shape.warp) {
+    for (const bool prof : {false, true}) {
+      const void* f = reinterpret_cast<const void*>(
+          g->packed ? (prof ? wbc_dev::bc_warp_kernel<true, true> : wbc_dev::bc_warp_kernel<true, false>)
+                    : (prof ? wbc_dev::bc_warp_kernel<false, true> : wbc_dev::bc_warp_kernel<false, false>));
+      WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(wbc_dev::WarpSmem))));
+    }
+    int per_sm = 0;
+    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, reinterpret_cast<const void*>(g->packed ? wbc_dev::bc_warp_kernel<true, false>
+                                                         : wbc_dev::bc_warp_kernel<false, false>),
+        32, sizeof(wbc_dev::WarpSmem)));
+    if (per_sm < 1) return set_error(WBC_E_CUDA, "warp kernel does not fit on an SM");
+    slots = per_sm * g->sm_count;
+  }
   if (team) {
     for (const bool prof : {false, true}) {
       const void* f = reinterpret_cast<const void*>(pick_team(shape.cluster, shape.threads, g->packed, prof));
@@ -271,28 +389,30 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
       WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(shape.dyn_smem)));
     }
-    cudaLaunchConfig_t cfg{};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = shape.cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(shape.cluster * g->sm_count, 1, 1);
-    cfg.blockDim = dim3(shape.threads, 1, 1);
-    cfg.dynamicSmemBytes = shape.dyn_smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int clusters = 0;
-    const void* fk = reinterpret_cast<const void*>(pick_team(shape.cluster, shape.threads, g->packed));
-    if (shape.cluster == 1) {  // plain launch: resident CTAs per SM x SMs
-      WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&clusters, fk, shape.threads, shape.dyn_smem));
-      clusters *= g->sm_count;
-    } else {
-      WBC_CUDA_TRY(cudaOccupancyMaxActiveClusters(&clusters, fk, &cfg));
+    if (!shape.warp) {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = shape.cluster;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(shape.cluster * g->sm_count, 1, 1);
+      cfg.blockDim = dim3(shape.threads, 1, 1);
+      cfg.dynamicSmemBytes = shape.dyn_smem;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      const void* fk = reinterpret_cast<const void*>(pick_team(shape.cluster, shape.threads, g->packed));
+      if (shape.cluster == 1) {  // plain launch: resident CTAs per SM x SMs
+        WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&clusters, fk, shape.threads, shape.dyn_smem));
+        clusters *= g->sm_count;
+      } else {
+        WBC_CUDA_TRY(cudaOccupancyMaxActiveClusters(&clusters, fk, &cfg));
+      }
+      if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
+      slots = clusters;
     }
-    if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
-    slots = clusters;
-  } else {
+  } else if (!shape.warp) {
     const KernelFn fn = pick_kernel(shape.threads, g->packed);
     for (const bool prof : {false, true})
       WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
@@ -308,50 +428,32 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   slots = std::max(1, std::min(slots, want));
   size_t free_b = 0, total_b = 0;
   WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  const uint64_t old_per_slot = ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (g->ws_team ? 20 : 0)) + dag_cap * 8;
-  uint64_t avail = free_b + (g->d_ws ? uint64_t(g->ws_slots) * old_per_slot : 0);
+  uint64_t avail = free_b + (g->d_ws ? g->ws_bytes : 0);
   const uint64_t reserve = (4ULL << 30) + total_b / 10;  // 4 GiB + 10% headroom
   avail = avail > reserve ? avail - reserve : 0;
   slots = static_cast<int>(std::min<uint64_t>(slots, std::max<uint64_t>(1, avail / per_slot)));
+  int rc = ensure_bytes(g, per_slot * slots);
+  if (rc) return rc;
   *slots_out = slots;
-  if (g->d_ws && g->ws_slots >= slots && (g->ws_team || !team)) return WBC_OK;
-  cudaFree(g->d_ws);
-  g->d_ws = nullptr;
-  g->ws_slots = 0;
-  void* base = nullptr;
-  const cudaError_t err = cudaMalloc(&base, per_slot * slots);
-  if (err != cudaSuccess)
-    return set_error(WBC_E_NOMEM, "workspace allocation of " + std::to_string(per_slot * slots) +
-                                      " bytes failed: " + cudaGetErrorString(err));
-  g->d_ws = base;
+  char* base = static_cast<char*>(g->d_ws);
+  g->last_warp = shape.warp;
+  if (shape.warp) {
+    // aborted sources re-run on one-warp teams over the same allocation
+    const uint64_t fb_per = ws_per_slot(g, false, true);
+    if (g->ws_bytes < fb_per) {
+      rc = ensure_bytes(g, fb_per);  // tiny workspaces: one fallback slot
+      if (rc) return rc;
+    }
+    carve_warp(g, static_cast<char*>(g->d_ws), slots);
+    g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
+    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true);
+    g->ws_slots = slots;
+    g->ws_team = false;
+    return WBC_OK;
+  }
+  g->ws = carve_cta_team(g, base, slots, team);
   g->ws_slots = slots;
   g->ws_team = team;
-  char* p = static_cast<char*>(base);
-  auto carve = [&](uint64_t bytes) {
-    char* q = p;
-    p += bytes * slots;
-    return q;
-  };
-  g->ws.n_stride = ns;
-  g->ws.dag_cap = dag_cap;
-  g->ws.sigma = reinterpret_cast<double*>(carve(ns * 8));
-  g->ws.delta = reinterpret_cast<double*>(carve(ns * 8));
-  g->ws.dag = reinterpret_cast<uint2*>(carve(dag_cap * 8));
-  g->ws.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  g->ws.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  g->ws.level_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  g->ws.near_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  g->ws.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  g->ws.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  if (team) {
-    g->ws.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    g->ws.ord_row = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    g->ws.epref = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    g->ws.near_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    g->ws.far_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  } else {
-    g->ws.ord_d = g->ws.ord_row = g->ws.epref = g->ws.near_q2 = g->ws.far_q2 = nullptr;
-  }
   return WBC_OK;
 }
 
@@ -403,7 +505,52 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_node_dev, 0, uint64_t{g->n} * 8, stream));
   if (g->profiling)
     WBC_CUDA_TRY(cudaMemsetAsync(g->d_prof, 0, sizeof(unsigned long long) * wbc_dev::kProfCounters, stream));
-  if (shape.cluster > 0) {
+  if (shape.warp) {
+    if (g->abort_cap < k) {
+      cudaFree(g->d_abort_list);
+      cudaError_t e2 = cudaSuccess;
+      g->d_abort_list = dev_alloc<uint32_t>(k, e2);
+      if (e2 != cudaSuccess) {
+        g->abort_cap = 0;
+        return set_error(WBC_E_NOMEM, "abort list allocation failed");
+      }
+      g->abort_cap = k;
+    }
+    if (!g->d_abort_count) {
+      cudaError_t e2 = cudaSuccess;
+      g->d_abort_count = dev_alloc<unsigned long long>(2, e2);
+      if (e2 == cudaSuccess) g->d_counter2 = dev_alloc<unsigned long long>(1, e2);
+      if (e2 != cudaSuccess) return set_error(WBC_E_NOMEM, "counter allocation failed");
+    }
+    wbc_dev::WarpParams w = g->wl;
+    w.g = p.g;
+    w.sources = d_sources;
+    w.k = k;
+    w.counter = g->d_counter;
+    w.node_bc = g->d_node_dev;
+    w.edge_bc = p.edge_bc;
+    w.depth = d_depth;
+    w.near_width = g->near_width;
+    w.inv = g->d_inv;
+    w.abort_list = g->d_abort_list;
+    w.abort_count = g->d_abort_count;
+    w.prof = p.prof;
+    if (!edge_bc) w.dag_slot = nullptr;
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_abort_count, 0, sizeof(unsigned long long), stream));
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter2, 0, sizeof(unsigned long long), stream));
+    const auto wk = g->packed ? (g->profiling ? wbc_dev::bc_warp_kernel<true, true> : wbc_dev::bc_warp_kernel<true, false>)
+                              : (g->profiling ? wbc_dev::bc_warp_kernel<false, true> : wbc_dev::bc_warp_kernel<false, false>);
+    wk<<<slots, 32, sizeof(wbc_dev::WarpSmem), stream>>>(w);
+    WBC_CUDA_TRY(cudaGetLastError());
+    // sources the warp kernel aborted: one-warp teams, count read on device
+    p.ws = g->ws_fb;
+    p.sources = g->d_abort_list;
+    p.k = k;
+    p.k_dev = g->d_abort_count;
+    p.counter = g->d_counter2;
+    pick_team(1, 32, g->packed, g->profiling)<<<g->fb_slots, 32, wbc_dev::team_dyn_smem(32), stream>>>(p);
+    WBC_CUDA_TRY(cudaGetLastError());
+  } else if (shape.cluster > 0) {
     // whole distance arrays of the few in-flight teams get evict-last
     if (g->tune_l2hot < 0) p.l2hot = g->n;
     cudaLaunchConfig_t cfg{};
@@ -427,10 +574,41 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
   g->stats[1] = shape.threads * std::max(1, shape.cluster);
-  g->last_kernel = shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
-                                           std::to_string(shape.cluster) + ">"
-                                     : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  g->stats[3] = 2;
+  g->last_kernel = shape.warp ? std::string("bc_warp_kernel")
+                  : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
+                                            std::to_string(shape.cluster) + ">"
+                                      : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
+  g->stats[3] = shape.warp ? 3 : 2;
+  return WBC_OK;
+}
+
+// Slot-0 state of the last single-source run: the warp kernel's layout, or
+// the team layout its aborted source was re-run on.
+struct Slot0 {
+  uint32_t* dist;
+  double* sigma;
+  double* delta;
+  uint32_t* order;
+  uint32_t* level_ends;
+  uint32_t* dag_ends;
+  uint2* dag;
+  bool warp_dag;   // dag entries are (pred, succ) instead of (slot, succ)
+  bool masked;     // distances carry kSettledBit
+};
+
+int slot0_state(wbc_gpu_graph* g, Slot0* out) {
+  const wbc_dev::Workspace& w = g->ws;
+  *out = Slot0{w.dist, w.sigma, w.delta, w.order, w.level_ends, w.dag_ends, w.dag, false, false};
+  if (!g->last_warp) return WBC_OK;
+  unsigned long long aborted = 0;
+  WBC_CUDA_TRY(cudaMemcpy(&aborted, g->d_abort_count, 8, cudaMemcpyDeviceToHost));
+  if (aborted) {
+    const wbc_dev::Workspace& f = g->ws_fb;
+    *out = Slot0{f.dist, f.sigma, f.delta, f.order, f.level_ends, f.dag_ends, f.dag, false, false};
+  } else {
+    const wbc_dev::WarpParams& l = g->wl;
+    *out = Slot0{l.dist, l.sigma, l.delta, l.order, l.level_ends, l.dag_ends, l.dag, true, true};
+  }
   return WBC_OK;
 }
 
@@ -642,6 +820,7 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "hot") g->tune_hot = value;
   else if (k == "l2hot") g->tune_l2hot = value;
   else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
+  else if (k == "warp") g->tune_warp = static_cast<int>(value);
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }
@@ -777,21 +956,26 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
     WBC_CUDA_TRY(cudaMemcpy(d_src, &source, 4, cudaMemcpyHostToDevice));
     WBC_CUDA_TRY(cudaMemset(d_scratch, 0, n * 8));
     WBC_CUDA_TRY(cudaMemset(d_dep, 0, n * 4));
-    WBC_CUDA_TRY(cudaMemset(g->ws.sigma, 0, n * 8));  // slot 0: unreached stay 0
-    WBC_CUDA_TRY(cudaMemset(g->ws.delta, 0, n * 8));
+    // slot 0's sigma and delta (identical offsets in every layout at one
+    // slot): unreached vertices stay 0
+    WBC_CUDA_TRY(cudaMemset(g->d_ws, 0, std::min<uint64_t>(g->ws_bytes, ws_ns(g) * 16)));
     int r = launch_run(g, d_src, 1, false, d_scratch, nullptr, d_dep, 0, true, true);
     if (r) return r;
     WBC_CUDA_TRY(cudaDeviceSynchronize());
-    WBC_CUDA_TRY(cudaMemcpy(du.data(), g->ws.dist, n * 4, cudaMemcpyDeviceToHost));
+    Slot0 st{};
+    if ((r = slot0_state(g, &st))) return r;
+    WBC_CUDA_TRY(cudaMemcpy(du.data(), st.dist, n * 4, cudaMemcpyDeviceToHost));
     if (dist)
-      for (uint64_t i = 0; i < n; ++i)
-        dist[g->perm[i]] = du[i] == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(du[i]);
+      for (uint64_t i = 0; i < n; ++i) {
+        const uint32_t d = (st.masked && du[i] != wbc_dev::kInfDist) ? (du[i] & wbc_dev::kDistMask) : du[i];
+        dist[g->perm[i]] = d == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(d);
+      }
     if (sigma) {
-      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), g->ws.sigma, n * 8, cudaMemcpyDeviceToHost));
+      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), st.sigma, n * 8, cudaMemcpyDeviceToHost));
       for (uint64_t i = 0; i < n; ++i) sigma[g->perm[i]] = tmp[i];
     }
     if (delta) {
-      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), g->ws.delta, n * 8, cudaMemcpyDeviceToHost));
+      WBC_CUDA_TRY(cudaMemcpy(tmp.data(), st.delta, n * 8, cudaMemcpyDeviceToHost));
       for (uint64_t i = 0; i < n; ++i) delta[g->perm[i]] = tmp[i];
     }
     if (depth) WBC_CUDA_TRY(cudaMemcpy(depth, d_dep + source, 4, cudaMemcpyDeviceToHost));
@@ -821,11 +1005,13 @@ int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t
   if (rc) return rc;
   unsigned int ov = 0;
   WBC_CUDA_TRY(cudaMemcpy(&ov, g->d_overflow, 4, cudaMemcpyDeviceToHost));
+  Slot0 st{};
+  if ((rc = slot0_state(g, &st))) return rc;
   std::vector<uint32_t> de(uint64_t{depth} + 1);
-  WBC_CUDA_TRY(cudaMemcpy(de.data(), g->ws.dag_ends, de.size() * 4, cudaMemcpyDeviceToHost));
-  const uint32_t len = std::min<uint64_t>(de[depth], g->ws.dag_cap);
+  WBC_CUDA_TRY(cudaMemcpy(de.data(), st.dag_ends, de.size() * 4, cudaMemcpyDeviceToHost));
+  const uint32_t len = std::min<uint64_t>(de[depth], st.warp_dag ? g->wl.dag_cap : g->ws.dag_cap);
   std::vector<uint2> d(len);
-  if (len) WBC_CUDA_TRY(cudaMemcpy(d.data(), g->ws.dag, uint64_t{len} * 8, cudaMemcpyDeviceToHost));
+  if (len) WBC_CUDA_TRY(cudaMemcpy(d.data(), st.dag, uint64_t{len} * 8, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> slots(g->packed ? 2ULL * g->m : 0);
   std::vector<uint2> slots64(g->packed ? 0 : 2ULL * g->m);
   if (g->m) {
@@ -835,7 +1021,7 @@ int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t
       WBC_CUDA_TRY(cudaMemcpy(slots64.data(), g->d_slots64, 16ULL * g->m, cudaMemcpyDeviceToHost));
   }
   for (uint32_t i = 0; i < len; ++i) {
-    const uint32_t u = g->packed ? slots[d[i].x] >> g->wbits : slots64[d[i].x].x;
+    const uint32_t u = st.warp_dag ? d[i].x : g->packed ? slots[d[i].x] >> g->wbits : slots64[d[i].x].x;
     pred[i] = g->perm[u];
     succ[i] = g->perm[d[i].y];
   }
@@ -853,11 +1039,13 @@ int wbc_gpu_sssp_levels(wbc_gpu_graph* g, uint32_t source, uint32_t* order, uint
   int rc = wbc_gpu_sssp_dump(g, source, nullptr, nullptr, nullptr, &depth);
   if (rc) return rc;
   // workspace slot 0 still holds the source's order / level ends
+  Slot0 st{};
+  if ((rc = slot0_state(g, &st))) return rc;
   std::vector<uint32_t> lev(uint64_t{depth} + 1);
-  WBC_CUDA_TRY(cudaMemcpy(lev.data(), g->ws.level_ends, lev.size() * 4, cudaMemcpyDeviceToHost));
+  WBC_CUDA_TRY(cudaMemcpy(lev.data(), st.level_ends, lev.size() * 4, cudaMemcpyDeviceToHost));
   const uint32_t len = lev[depth];
   std::vector<uint32_t> ord(len);
-  if (len) WBC_CUDA_TRY(cudaMemcpy(ord.data(), g->ws.order, uint64_t{len} * 4, cudaMemcpyDeviceToHost));
+  if (len) WBC_CUDA_TRY(cudaMemcpy(ord.data(), st.order, uint64_t{len} * 4, cudaMemcpyDeviceToHost));
   for (uint32_t i = 0; i < len; ++i) order[i] = g->perm[ord[i]];
   std::memcpy(level_ends, lev.data(), lev.size() * 4);
   *order_len = len;

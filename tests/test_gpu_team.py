@@ -15,8 +15,9 @@ from test_gpu_parity import assert_close, check_graph
 
 pytestmark = pytest.mark.gpu
 
-# cluster size; "w" = one warp (32-thread CTA) per source
-CLUSTERS = (1, 2, 4, 8, 16, "w")
+# cluster size; "w" = one-warp teams (32-thread CTA per source); "k" = the
+# one-warp kernel with on-chip near set (bc_warp.cuh) and its team fallback
+CLUSTERS = (1, 2, 4, 8, 16, "w", "k")
 
 
 def team_graph(W, g, c):
@@ -24,6 +25,8 @@ def team_graph(W, g, c):
     if c == "w":
         gg.set_param("cluster", 1)
         gg.set_param("threads", 32)
+    elif c == "k":
+        gg.set_param("warp", 2)
     else:
         gg.set_param("cluster", c)
     return gg
@@ -68,7 +71,7 @@ def test_team_race_and_dump(W, oracle, c):
 
 @pytest.mark.parametrize("c", CLUSTERS)
 def test_team_random_equivalence(W, oracle, c):
-    rng = np.random.default_rng(1234 + (c if c != "w" else 99))
+    rng = np.random.default_rng(1234 + (c if isinstance(c, int) else ord(c)))
     for i in range(12):
         seed = int(rng.integers(1, 2**62))
         if i % 2 == 0:
@@ -95,7 +98,7 @@ def test_team_hub_rows_and_sampled(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8, "w"))
+@pytest.mark.parametrize("c", (1, 8, "w", "k"))
 def test_team_dag_overflow_fallback(W, oracle, c):
     a = 60
     g = F.graph_of([(i, a + j, 1.0) for i in range(a) for j in range(a)])
@@ -105,7 +108,7 @@ def test_team_dag_overflow_fallback(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (2, 16, "w"))
+@pytest.mark.parametrize("c", (2, 16, "w", "k"))
 def test_team_unpacked_slots(W, oracle, c):
     el = W.gen_er(3000, 6.0, 7)
     el.w = (np.random.default_rng(7).integers(1, 1_100_000, len(el))).astype(np.float64)
@@ -116,11 +119,55 @@ def test_team_unpacked_slots(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8, "w"))
+@pytest.mark.parametrize("c", (1, 8, "w", "k"))
 def test_team_grid_large_diameter(W, oracle, c):
     el = W.assign_weights(W.gen_grid(64, 64), 1, 1000, 1)
     g = W.build_csr(el)
     src = W.sample_sources(g.n, 12, 1)
     gg = team_graph(W, g, c)
     check_graph(W, oracle, g, gg=gg, sources=src, edge=True)
+    gg.close()
+
+
+def test_warp_kernel_aborts_fall_back(W, oracle):
+    """Hub rows give levels of thousands of vertices: the one-warp kernel
+    aborts those sources and the team kernel recomputes them (same stream)."""
+    el = W.assign_weights(W.gen_kronecker(12, 32.0, 4), 1, 255, 4)
+    g = W.build_csr(el)
+    gg = team_graph(W, g, "k")
+    src = W.sample_sources(g.n, 24, 3)
+    check_graph(W, oracle, g, gg=gg, sources=src, edge=True)
+    assert gg.last_kernel() == "bc_warp_kernel"
+    gg.close()
+
+
+def test_warp_kernel_grid_levels_and_dag(W, oracle):
+    """Large-diameter grid on the one-warp kernel: level sets and the
+    recorded DAG per level equal the oracle's Eq. 4 structure."""
+    el = W.assign_weights(W.gen_grid(48, 40), 1, 1000, 2)
+    g = W.build_csr(el)
+    gg = team_graph(W, g, "k")
+    off, adj, wt = g.offsets, g.adjacency, g.weights
+    for s in (0, 777, g.n - 1):
+        o = oracle.eq4_source(g, s)
+        ol = [np.sort(o["order"][o["ends"][i]:o["ends"][i + 1]]) for i in range(len(o["ends"]) - 1)]
+        lv = gg.levels(s)
+        assert len(lv) == len(ol) and all(np.array_equal(a, b) for a, b in zip(lv, ol))
+        segs, ov = gg.dag(s)
+        assert not ov
+        dist = o["dist"]
+        for L, lvl in enumerate(ol):
+            want = sorted((int(adj[e]), int(x)) for x in lvl for e in range(off[x], off[x + 1])
+                          if dist[adj[e]] + wt[e] == dist[x])
+            got = sorted(zip(segs[L][0].tolist(), segs[L][1].tolist()))
+            assert got == want, f"s={s} level {L}"
+    gg.close()
+
+
+def test_warp_kernel_distance_bound_aborts(W, oracle):
+    """Distances past 2^31 do not fit beside the settled bit: the one-warp
+    kernel aborts and the team kernel (u32 distances) finishes the source."""
+    g = F.graph_of([(i, i + 1, 30_000_000.0) for i in range(99)])  # path: d reaches 2.97e9
+    gg = team_graph(W, g, "k")
+    check_graph(W, oracle, g, gg=gg, sources=[0, 5, 99], edge=True)
     gg.close()

@@ -42,6 +42,7 @@ for rep in range(a.reps):
         pc = gg.profile_counters(); k = len(src)
         print("  per source: " + ", ".join(f"{kk}={v/k:.4g}" for kk, v in pc.items()) + f"  (2m={2*g.m})", flush=True)
         cyc = {kk: v for kk, v in pc.items() if kk.startswith("cyc_")}
+        print("  aborts:", {kk: v for kk, v in pc.items() if kk.startswith("abort_")}, flush=True)
         tot = sum(cyc.values()) or 1
         print("  phase share: " + ", ".join(f"{kk[4:]}={100*v/tot:.1f}%" for kk, v in cyc.items()) +
               f"; per-CTA ms/source at 1.9GHz = {tot/k/1.9e6:.2f}", flush=True)
