@@ -14,6 +14,7 @@
 // The implementation differs: one pass with an open-addressing interner
 // instead of std::unordered_map, and a pre-sized slot fill.
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <cmath>
 #include <cstdio>
@@ -24,6 +25,7 @@
 #include <ostream>
 
 #include "host_hash.hpp"
+#include "host_parallel.hpp"
 #include "wbc/graph.hpp"
 
 namespace wbc {
@@ -114,8 +116,193 @@ EdgeList parse_edge_list(std::istream& in, double default_weight) {
   return parse_edge_list_text(text.data(), text.size(), default_weight);
 }
 
+namespace {
+
+// Parallel build_csr with output identical to the serial one (the
+// reference's graph.cpp:75-133): dense ids by first appearance over the
+// (u, v) sequence, canonical edges by first occurrence keeping that
+// occurrence's orientation and the minimum weight, rows filled in edge-id
+// order.  Only for raw ids below 2^32 and not far above the entry count
+// (direct first-appearance table); returns false otherwise.
+bool build_csr_parallel(const EdgeList& edges, CsrGraph& g) {
+  const std::size_t len = edges.entries.size();
+  const unsigned T = detail::host_threads();
+  RawId max_raw = 0;
+  for (const WeightedEdge& e : edges.entries) max_raw = std::max({max_raw, e.u, e.v});
+  if (max_raw >= 0xFFFFFFFFULL || max_raw > 8 * len + (1u << 20) || 2 * len >= 0xFFFFFFFFULL) return false;
+  const std::size_t R = static_cast<std::size_t>(max_raw) + 1;
+  constexpr std::uint32_t kNone = 0xFFFFFFFFu;
+  // 1. first appearance of every raw id (position 2i for u, 2i+1 for v)
+  std::vector<std::atomic<std::uint32_t>> first(R);
+  detail::parallel_chunks(R, T, [&](unsigned, std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t i = b; i < e; ++i) first[i].store(kNone, std::memory_order_relaxed);
+  });
+  auto amin = [](std::atomic<std::uint32_t>& a, std::uint32_t v) {
+    std::uint32_t cur = a.load(std::memory_order_relaxed);
+    while (v < cur && !a.compare_exchange_weak(cur, v, std::memory_order_relaxed)) {
+    }
+  };
+  detail::parallel_chunks(len, T, [&](unsigned, std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t i = b; i < e; ++i) {
+      amin(first[edges.entries[i].u], static_cast<std::uint32_t>(2 * i));
+      amin(first[edges.entries[i].v], static_cast<std::uint32_t>(2 * i + 1));
+    }
+  });
+  std::vector<std::pair<std::uint32_t, std::uint32_t>> order;  // (first position, raw)
+  order.reserve(len < R ? 2 * len : R);
+  for (std::size_t r = 0; r < R; ++r) {
+    const std::uint32_t f = first[r].load(std::memory_order_relaxed);
+    if (f != kNone) order.emplace_back(f, static_cast<std::uint32_t>(r));
+  }
+  std::sort(order.begin(), order.end());
+  std::vector<NodeId> dense(R, kNone);
+  g.original_id.resize(order.size());
+  for (std::size_t k = 0; k < order.size(); ++k) {
+    dense[order[k].second] = static_cast<NodeId>(k);
+    g.original_id[k] = order[k].second;
+  }
+  std::vector<std::atomic<std::uint32_t>>().swap(first);
+  g.n = static_cast<NodeId>(order.size());
+  const std::size_t n = g.n;
+  // 2. canonical edges: group occurrences by the smaller endpoint (stable
+  //    counting sort), find each key's first occurrence and minimum weight
+  std::vector<std::uint32_t> cnt(static_cast<std::size_t>(T) * n, 0);
+  detail::parallel_chunks(len, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint32_t* c = cnt.data() + static_cast<std::size_t>(t) * n;
+    for (std::uint64_t i = b; i < e; ++i) {
+      const NodeId a = dense[edges.entries[i].u], bb = dense[edges.entries[i].v];
+      if (a != bb) ++c[std::min(a, bb)];
+    }
+  });
+  std::vector<std::uint64_t> gstart(n + 1, 0);
+  for (std::size_t x = 0; x < n; ++x) {  // exclusive positions, thread-major within a group
+    std::uint64_t acc = gstart[x];
+    for (unsigned t = 0; t < T; ++t) {
+      const std::uint32_t c = cnt[static_cast<std::size_t>(t) * n + x];
+      cnt[static_cast<std::size_t>(t) * n + x] = static_cast<std::uint32_t>(acc - gstart[x]);
+      acc += c;
+    }
+    gstart[x + 1] = acc;
+  }
+  const std::uint64_t valid = gstart[n];
+  std::vector<std::uint32_t> gidx(valid);  // entry index, grouped by smaller endpoint, in entry order
+  detail::parallel_chunks(len, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint32_t* c = cnt.data() + static_cast<std::size_t>(t) * n;
+    for (std::uint64_t i = b; i < e; ++i) {
+      const NodeId a = dense[edges.entries[i].u], bb = dense[edges.entries[i].v];
+      if (a == bb) continue;
+      const NodeId lo = std::min(a, bb);
+      gidx[gstart[lo] + c[lo]++] = static_cast<std::uint32_t>(i);
+    }
+  });
+  std::vector<std::uint8_t> keep(len, 0);
+  std::vector<double> wmin(len, 0.0);
+  std::atomic<std::uint64_t> merged{0};
+  detail::parallel_chunks(n, T, [&](unsigned, std::uint64_t b, std::uint64_t e) {
+    std::vector<std::pair<NodeId, std::uint32_t>> grp;
+    std::uint64_t mloc = 0;
+    for (std::uint64_t x = b; x < e; ++x) {
+      grp.clear();
+      for (std::uint64_t k = gstart[x]; k < gstart[x + 1]; ++k) {
+        const std::uint32_t i = gidx[k];
+        const NodeId a = dense[edges.entries[i].u], bb = dense[edges.entries[i].v];
+        grp.emplace_back(std::max(a, bb), i);
+      }
+      std::sort(grp.begin(), grp.end());  // by other endpoint, then entry index
+      for (std::size_t k = 0; k < grp.size();) {
+        std::size_t j = k;
+        double w = edges.entries[grp[k].second].w;
+        while (++j < grp.size() && grp[j].first == grp[k].first) w = std::min(w, edges.entries[grp[j].second].w);
+        keep[grp[k].second] = 1;
+        wmin[grp[k].second] = w;
+        mloc += j - k - 1;
+        k = j;
+      }
+    }
+    merged += mloc;
+  });
+  std::vector<std::uint32_t>().swap(gidx);
+  g.merged_duplicates = merged.load();
+  // edge id of a first occurrence = number of first occurrences before it
+  std::vector<std::uint64_t> part(T + 1, 0);
+  detail::parallel_chunks(len, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint64_t c = 0;
+    for (std::uint64_t i = b; i < e; ++i) c += keep[i];
+    part[t + 1] = c;
+  });
+  for (unsigned t = 0; t < T; ++t) part[t + 1] += part[t];
+  g.m = static_cast<EdgeId>(part[T]);
+  const std::size_t m = g.m;
+  g.edge_u.resize(m);
+  g.edge_v.resize(m);
+  std::vector<double> edge_w(m);
+  detail::parallel_chunks(len, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint64_t id = part[t];
+    for (std::uint64_t i = b; i < e; ++i)
+      if (keep[i]) {
+        g.edge_u[id] = dense[edges.entries[i].u];
+        g.edge_v[id] = dense[edges.entries[i].v];
+        edge_w[id] = wmin[i];
+        ++id;
+      }
+  });
+  std::vector<std::uint8_t>().swap(keep);
+  std::vector<double>().swap(wmin);
+  std::vector<NodeId>().swap(dense);
+  // 3. rows in edge-id order: stable counting sort of the 2m (vertex, edge)
+  //    incidences, per-thread counts over contiguous edge ranges
+  std::fill(cnt.begin(), cnt.end(), 0u);
+  detail::parallel_chunks(m, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint32_t* c = cnt.data() + static_cast<std::size_t>(t) * n;
+    for (std::uint64_t k = b; k < e; ++k) {
+      ++c[g.edge_u[k]];
+      ++c[g.edge_v[k]];
+    }
+  });
+  g.offsets.assign(n + 1, 0);
+  for (std::size_t x = 0; x < n; ++x) {
+    std::uint64_t acc = g.offsets[x];
+    for (unsigned t = 0; t < T; ++t) {
+      const std::uint32_t c = cnt[static_cast<std::size_t>(t) * n + x];
+      cnt[static_cast<std::size_t>(t) * n + x] = static_cast<std::uint32_t>(acc);
+      acc += c;
+    }
+    g.offsets[x + 1] = static_cast<EdgeId>(acc);
+  }
+  const std::size_t slots = 2 * m;
+  g.adjacency.resize(slots);
+  g.weights.resize(slots);
+  g.edge_id.resize(slots);
+  detail::parallel_chunks(m, T, [&](unsigned t, std::uint64_t b, std::uint64_t e) {
+    std::uint32_t* c = cnt.data() + static_cast<std::size_t>(t) * n;
+    for (std::uint64_t k = b; k < e; ++k) {
+      const NodeId a = g.edge_u[k], bb = g.edge_v[k];
+      const std::uint32_t sa = c[a]++, sb = c[bb]++;
+      g.adjacency[sa] = bb;
+      g.weights[sa] = edge_w[k];
+      g.edge_id[sa] = static_cast<EdgeId>(k);
+      g.adjacency[sb] = a;
+      g.weights[sb] = edge_w[k];
+      g.edge_id[sb] = static_cast<EdgeId>(k);
+    }
+  });
+  g.min_incident_weight.assign(n, kInf);
+  detail::parallel_chunks(n, T, [&](unsigned, std::uint64_t b, std::uint64_t e) {
+    for (std::uint64_t x = b; x < e; ++x)
+      for (EdgeId s = g.offsets[x]; s < g.offsets[x + 1]; ++s)
+        g.min_incident_weight[x] = std::min(g.min_incident_weight[x], g.weights[s]);
+  });
+  return true;
+}
+
+}  // namespace
+
 CsrGraph build_csr(const EdgeList& edges) {
   CsrGraph g;
+  if (edges.entries.size() >= detail::parallel_min_entries() && detail::host_threads() > 1) {
+    CsrGraph p;
+    if (build_csr_parallel(edges, p)) return p;
+  }
   const std::size_t len = edges.entries.size();
   detail::U64Map dense(std::min<std::size_t>(2 * len, 1u << 20));
   detail::U64Map seen(std::min<std::size_t>(len, 1u << 20));

@@ -227,23 +227,24 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
   }
-  // Skewed graphs run on the team kernel (bc_team.cuh).  One CTA per source
-  // while 148 distance arrays fit in half of L2 (BA-65536: 24.4 vs 18.0
-  // GTEPS for the per-CTA kernel), else two-CTA clusters, halving the
-  // in-flight distance footprint (R-MAT-20: 37.1 vs 34.4; C=4 strands 16
-  // SMs, 36.3).  Measured on B200, DESIGN.md §4.
+  // Skewed graphs run on the team kernel (bc_team.cuh), with the smallest
+  // cluster whose in-flight distance arrays stay near L2 size: one CTA per
+  // source while 148 of them fit in 64 MB (BA-65536: 27.5 vs 18.0 GTEPS for
+  // the per-CTA kernel), else the smallest C in {2,4,8,16} with
+  // (148/C) * 4n <= 256 MB (R-MAT-20: C=2, 43 GTEPS; R-MAT-24: C=16, 32.8
+  // vs 21.8 at C=2).  Measured on B200, DESIGN.md §4.
   if (g->tune_cluster < 0 && !tiny && g->hot_coverage_25k >= 0.4) {
-    s.cluster = n * 4 * static_cast<uint64_t>(g->sm_count) <= (64ULL << 20) ? 1 : 2;
+    const uint64_t per = n * 4;
+    int c = 1;
+    if (per * static_cast<uint64_t>(g->sm_count) > (64ULL << 20)) {
+      c = 2;
+      while (c < 16 && per * static_cast<uint64_t>(g->sm_count / c) > (256ULL << 20)) c *= 2;
+    }
+    s.cluster = c;
     s.threads = 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
   }
-  if (g->tune_threads)
-    s.threads = g->tune_threads <= 128 ? 128 : g->tune_threads <= 256 ? 256 : g->tune_threads <= 512 ? 512 : 1024;
-  else if (!tiny && g->hot_coverage_25k >= 0.4)
-    s.threads = 1024;
-  else
-    s.threads = 128;
   // Flat, large graphs (grid / road-like: latency-bound rounds, small
   // frontiers): one warp per source (grid-2048: 1.56 vs 1.1 GTEPS for the
   // 128-thread per-CTA kernel).  Tiny graphs keep the per-CTA kernel with

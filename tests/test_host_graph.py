@@ -123,3 +123,40 @@ def test_parser_matches_reference():
     with pytest.raises(ValueError):
         W.parse_edge_list("0 1", 0.0)                                        # default weight > 0
     assert len(W.parse_edge_list(io.StringIO("0 1 2\n"))) == 1              # stream input
+
+
+_PAR_SCRIPT = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1701_05975_b200 as W
+el = W.assign_weights(W.gen_kronecker(13, 24.0, 5), 1, 9, 5)
+# duplicates (min weight wins, first orientation kept), reversed pairs and sparse raw ids
+u = np.concatenate([el.u, el.v[:500], el.u[:300] * 7 + 11])
+v = np.concatenate([el.v, el.u[:500], el.v[:300] * 7 + 11])
+w = np.concatenate([el.w, np.full(500, 0.5), el.w[:300]])
+e2 = W.EdgeList(); e2.u, e2.v, e2.w = u.astype(np.uint64), v.astype(np.uint64), w
+g = W.build_csr(e2)
+np.savez(sys.argv[2], gu=el.u, gv=el.v, gw=el.w, off=g.offsets, adj=g.adjacency, wt=g.weights, eid=g.edge_id,
+         mw=g.min_incident_weight, oid=g.original_id, eu=g.edge_u, ev=g.edge_v, merged=[g.merged_duplicates])
+'''
+
+
+def test_parallel_builders_identical_to_serial(tmp_path):
+    """gen_kronecker and build_csr take thread-parallel paths above
+    WBC_HOST_PARALLEL_MIN; their output must equal the serial paths
+    (the reference's stream and first-appearance orders) array for array."""
+    import subprocess
+    import sys
+    from conftest import ROOT
+    script = tmp_path / "par.py"
+    script.write_text(_PAR_SCRIPT)
+    res = {}
+    for mode, thr in (("serial", str(1 << 40)), ("parallel", "1000")):
+        out = tmp_path / f"{mode}.npz"
+        env = dict(os.environ, WBC_HOST_PARALLEL_MIN=thr, WBC_HOST_THREADS="4")
+        subprocess.run([sys.executable, str(script), ROOT, str(out)], env=env, check=True)
+        res[mode] = np.load(out)
+    a, b = res["serial"], res["parallel"]
+    for k in a.files:
+        assert np.array_equal(a[k], b[k]), k
+    assert a["merged"][0] > 0
