@@ -56,8 +56,10 @@ __device__ __forceinline__ void team_red_reset(TeamRed& r) {
   r.flags = 0;
 }
 
-// Frontier vertices staged per chunk: at least 128, so a one-warp team
+// Frontier vertices staged per chunk: T, and at least 128 so a one-warp team
 // relaxes a typical large-diameter level (~50 vertices) in one chunk.
+// (4096-vertex chunks for T = 1024 measured 2.4x SLOWER: the larger shared
+// footprint shrinks L1 to ~30 KB and the kernel's register spills thrash.)
 template <int T>
 constexpr int team_chunk() { return T < 128 ? 128 : T; }
 
@@ -121,7 +123,14 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
 // 5 arrays of kTeamQ u32 per warp; a warp holds < 32 entries between drains
 // and adds at most 32 * kUnroll per step.
 constexpr uint32_t kTeamQ = 32 * kUnroll + 32;
-__host__ __device__ constexpr size_t team_dyn_smem(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
+__host__ __device__ constexpr size_t team_q_bytes(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
+template <int T>
+constexpr size_t team_sh_bytes() { return (sizeof(TeamShared<T>) + 15) / 16 * 16; }
+// Dynamic shared memory of a team CTA: the staged chunk + phase ring, then the
+// per-warp queues.
+inline size_t team_dyn_smem(int threads) {
+  return threads <= 32 ? team_sh_bytes<32>() + team_q_bytes(32) : team_sh_bytes<1024>() + team_q_bytes(1024);
+}
 
 // 1024-thread CTAs: one per SM.  32-thread CTAs (one warp per source, for
 // large-diameter graphs whose rounds are latency-bound): 16 per SM, 128 regs.
@@ -129,8 +138,9 @@ constexpr int team_min_blocks(int threads) { return threads >= 1024 ? 1 : (threa
 
 template <int T, int C, bool PACKED, bool PROF>
 __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const RunParams p) {
-  __shared__ TeamShared<T> sh;
-  extern __shared__ uint32_t team_q[];
+  extern __shared__ __align__(16) unsigned char team_raw[];
+  TeamShared<T>& sh = *reinterpret_cast<TeamShared<T>*>(team_raw);
+  uint32_t* const team_q = reinterpret_cast<uint32_t*>(team_raw + team_sh_bytes<T>());
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   uint32_t rank = 0;
@@ -287,10 +297,12 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             uint32_t ce;
             const int cnt = stage(j, fe, cb, my_e, Ee, ce);
             const uint32_t total = ce - cb;
+            // one contiguous edge range per warp (measured: handing out
+            // 128-edge blocks dynamically was not faster)
             uint32_t wb, we;
+            const uint32_t lane = tid & 31;
             if (warp_range<T>(total, wb, we)) {
               int j0 = find_row(sh.pref, cnt, wb);
-              const uint32_t lane = tid & 31;
               const uint32_t lt = (1u << lane) - 1u;
               uint32_t* const q = team_q + (tid >> 5) * (5 * kTeamQ);
               uint32_t* const qiu = q;               // improvement candidates: u
@@ -393,12 +405,13 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
               };
               fetch(wb);
               for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
+                const uint32_t cwe = we;
                 uint32_t du[kUnroll];
                 Word cx[kUnroll];
                 int cj[kUnroll];
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
-                  const bool valid = e0 + 32 * k + lane < we;
+                  const bool valid = e0 + 32 * k + lane < cwe;
                   du[k] = valid ? dist.load(nbr(xw[k])) : 0u;
                   cx[k] = xw[k];
                   cj[k] = jj[k];
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
                   const uint32_t e = e0 + 32 * k + lane;
-                  const bool valid = e < we;
+                  const bool valid = e < cwe;
                   const uint32_t dv = sh.dv[cj[k]];
                   const uint32_t u = nbr(cx[k]), w = wgt(cx[k]);
                   const uint32_t nd = dv + w;

@@ -134,6 +134,7 @@ struct wbc_gpu_graph {
   int tune_slots = 0;
   int64_t tune_hot = -1;
   int64_t tune_l2hot = -1;
+  bool tune_near = false;      // near_width set explicitly (else the launch shape may adjust it)
   int tune_warp = 0;           // 1: bc_warp_kernel for flat graphs, 2: always (tests)
   int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
   bool ws_team = false;        // workspace carries the team-kernel arrays
@@ -190,6 +191,7 @@ KernelFn pick_team(int c, int threads, bool packed, bool prof = false) {
 }
 
 struct LaunchShape {
+  uint32_t near_width = 0; // 0: the graph's automatic width
   bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
   int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
   int threads = 128;
@@ -243,6 +245,10 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.cluster = c;
     s.threads = 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
+    // near window: flat optimum around 8-16 on skewed graphs (R-MAT-20 45.2
+    // GTEPS at 8 vs 44.6 at the automatic 18; BA 30.4 at 8 vs 28.7 at 2;
+    // R-MAT-24 33.8 at 8 vs 32.9 at 19)
+    if (!g->tune_near) s.near_width = std::min<uint32_t>(16, std::max<uint32_t>(8, g->near_width));
     return s;
   }
   // Flat, large graphs (grid / road-like: latency-bound rounds, small
@@ -490,7 +496,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   p.node_bc = g->d_node_dev;
   p.edge_bc = edge_bc ? d_edge : nullptr;
   p.depth = d_depth;
-  p.near_width = g->near_width;
+  p.near_width = shape.near_width ? shape.near_width : g->near_width;
   p.overflow = g->d_overflow;
   p.keep_state = keep_state ? 1 : 0;
   p.inv = g->d_inv;
@@ -531,7 +537,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     w.node_bc = g->d_node_dev;
     w.edge_bc = p.edge_bc;
     w.depth = d_depth;
-    w.near_width = g->near_width;
+    w.near_width = p.near_width;
     w.inv = g->d_inv;
     w.abort_list = g->d_abort_list;
     w.abort_count = g->d_abort_count;
@@ -808,7 +814,10 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uin
   g->tune_threads = threads_per_cta;
   g->tune_slots = max_slots;
   g->tune_hot = hot_vertices;
-  if (near_width) g->near_width = near_width;
+  if (near_width) {
+    g->near_width = near_width;
+    g->tune_near = true;
+  }
   return WBC_OK;
 }
 
@@ -817,7 +826,10 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   const std::string k = name;
   if (k == "threads") g->tune_threads = static_cast<int>(value);
   else if (k == "slots") g->tune_slots = static_cast<int>(value);
-  else if (k == "near_width") g->near_width = value > 0 ? static_cast<uint32_t>(value) : g->near_width;
+  else if (k == "near_width") {
+    g->near_width = value > 0 ? static_cast<uint32_t>(value) : g->near_width;
+    g->tune_near = value > 0;
+  }
   else if (k == "hot") g->tune_hot = value;
   else if (k == "l2hot") g->tune_l2hot = value;
   else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
