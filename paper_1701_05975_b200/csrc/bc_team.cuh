@@ -84,14 +84,18 @@ __device__ __forceinline__ uint32_t team_append(uint32_t* counter) {
   return base + grp.thread_rank();
 }
 
-// Distances of a team's source: few sources are in flight, so every entry
-// carries the evict-last hint (no per-access branch).
+// Distances of a team's source: ids below `hot` (the degree-descending
+// relabel puts the most-gathered vertices first) carry the L2 evict-last
+// hint, the rest evict-normal; the policy is selected per access in a
+// register (no branch).  hot = n marks every entry.
 struct TeamDist {
   uint32_t* gl;
-  uint64_t keep;
-  __device__ __forceinline__ uint32_t load(uint32_t u) const { return ld_cg_hint(gl + u, keep); }
+  uint64_t keep, norm;
+  uint32_t hot;
+  __device__ __forceinline__ uint64_t pol(uint32_t u) const { return u < hot ? keep : norm; }
+  __device__ __forceinline__ uint32_t load(uint32_t u) const { return ld_cg_hint(gl + u, pol(u)); }
   __device__ __forceinline__ uint32_t fetch_min(uint32_t u, uint32_t v) const {
-    return atom_min_hint(gl + u, v, keep);
+    return atom_min_hint(gl + u, v, pol(u));
   }
 };
 
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
   const uint64_t off = static_cast<uint64_t>(team) * p.ws.n_stride;
   const uint64_t keep_pol = l2_policy_evict_last();
   const uint64_t stream_pol = l2_policy_evict_first();
-  const TeamDist dist{p.ws.dist + off, keep_pol};
+  const TeamDist dist{p.ws.dist + off, keep_pol, l2_policy_evict_normal(), p.l2hot};
   double* const sigma = p.ws.sigma + off;
   double* const delta = p.ws.delta + off;
   uint32_t* const order = p.ws.order + off;

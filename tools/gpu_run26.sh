@@ -1,0 +1,2 @@
+timeout 600 python tools/probe_multi.py --graph rmat20 --k 592 --clusters 2 --nears 16 --l2hots -1,300000,150000 2>&1 | tail -3
+timeout 2400 python tools/probe_multi.py --graph rmat24 --k 296 --clusters 8,16 --nears 8 --l2hots -1,4000000,2000000,1000000 2>&1 | tail -9
