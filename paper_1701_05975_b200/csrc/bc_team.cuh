@@ -23,7 +23,9 @@
 //    sigma accesses of all its unrolled groups before consuming any of them;
 //    queue appends are ballot-aggregated, one atomic per queue per warp step;
 //  * the near/far queues are ping-pong buffers (in-place compaction across
-//    CTAs would race);
+//    warps would race; one-warp teams get the same buffer twice, which is
+//    safe because a warp step reads all its entries before it writes and a
+//    write position never passes a read position);
 //  * team scalars (queue append counters, Delta minima, the next source
 //    index) live in a ring of 4 slots in rank 0's shared memory (DSMEM):
 //    phase p appends/reduces into slot p%4, every thread reads slot p%4 right

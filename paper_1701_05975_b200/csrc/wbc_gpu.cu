@@ -296,13 +296,16 @@ uint64_t ws_dcap(const wbc_gpu_graph* g, bool warp) {
   const uint64_t n = g->n;
   return warp ? round_up(n + n / 8 + 1024, 64) : round_up(n + n / 2 + 1024, 64);
 }
-uint64_t ws_per_slot(const wbc_gpu_graph* g, bool warp, bool team) {
+uint64_t ws_per_slot(const wbc_gpu_graph* g, bool warp, bool team, bool one_warp = false) {
   const uint64_t ns = ws_ns(g);
   if (warp) return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4) + ws_dcap(g, true) * 12;
-  return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? 20 : 0)) + ws_dcap(g, false) * 8;
+  // one-warp teams compact their queues in place (a step reads its entries
+  // before it writes, and writes never pass reads): no second buffers
+  return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? (one_warp ? 12 : 20) : 0)) + ws_dcap(g, false) * 8;
 }
 
-wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slots, bool team) {
+wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slots, bool team,
+                                  bool one_warp = false) {
   const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g, false);
   auto carve = [&](uint64_t bytes) {
     char* q = p;
@@ -325,8 +328,8 @@ wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slot
     w.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
     w.ord_row = reinterpret_cast<uint32_t*>(carve(ns * 4));
     w.epref = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    w.near_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
-    w.far_q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.near_q2 = one_warp ? w.near_q : reinterpret_cast<uint32_t*>(carve(ns * 4));
+    w.far_q2 = one_warp ? w.far_q : reinterpret_cast<uint32_t*>(carve(ns * 4));
   }
   return w;
 }
@@ -370,7 +373,8 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   const bool team = shape.cluster > 0;
-  const uint64_t per_slot = ws_per_slot(g, shape.warp, team);
+  const bool one_warp = team && shape.cluster == 1 && shape.threads <= 32;
+  const uint64_t per_slot = ws_per_slot(g, shape.warp, team, one_warp);
   int slots = 0;
   if (shape.warp) {
     for (const bool prof : {false, true}) {
@@ -446,19 +450,19 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   g->last_warp = shape.warp;
   if (shape.warp) {
     // aborted sources re-run on one-warp teams over the same allocation
-    const uint64_t fb_per = ws_per_slot(g, false, true);
+    const uint64_t fb_per = ws_per_slot(g, false, true, true);
     if (g->ws_bytes < fb_per) {
       rc = ensure_bytes(g, fb_per);  // tiny workspaces: one fallback slot
       if (rc) return rc;
     }
     carve_warp(g, static_cast<char*>(g->d_ws), slots);
     g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
-    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true);
+    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
     g->ws_slots = slots;
     g->ws_team = false;
     return WBC_OK;
   }
-  g->ws = carve_cta_team(g, base, slots, team);
+  g->ws = carve_cta_team(g, base, slots, team, one_warp);
   g->ws_slots = slots;
   g->ws_team = team;
   return WBC_OK;
