@@ -1,0 +1,37 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck /
+racecheck / synccheck).  Each case is checked against the oracle too.
+
+    compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+
+import paper_1701_05975_b200 as W  # noqa: E402
+from oracle import Oracle  # noqa: E402
+
+O = Oracle()
+tol = lambda a, b: np.abs(a - b) <= np.maximum(1e-12, 1e-9 * np.maximum(np.abs(a), np.abs(b)))  # noqa: E731
+kron = W.build_csr(W.assign_weights(W.gen_kronecker(11, 16.0, 3), 1, 255, 3))
+grid = W.build_csr(W.assign_weights(W.gen_grid(24, 24), 1, 1000, 3))
+cases = [("per-CTA kernel (tiny graph)", kron, {}),
+         ("team C=1", kron, {"cluster": 1}),
+         ("team C=2", kron, {"cluster": 2}),
+         ("team C=4", kron, {"cluster": 4}),
+         ("one-warp team", grid, {"cluster": 1, "threads": 32}),
+         ("warp kernel + fallback", kron, {"warp": 2}),
+         ("warp kernel", grid, {"warp": 2})]
+for name, g, params in cases:
+    src = W.sample_sources(g.n, 6, 1)
+    gg = W.GpuGraph(g, 0)
+    for k, v in params.items():
+        gg.set_param(k, v)
+    r = gg.bc(W.EngineOptions(sources=src, compute_edge_bc=True))
+    kern = gg.last_kernel()
+    gg.close()
+    node, edge, depth = O.bc_eq4(g, sources=src, edge_bc=True)
+    ok = tol(r.node_bc, node).all() and tol(r.edge_bc, edge).all() and np.array_equal(r.depth_per_source, depth)
+    print(f"{name:28s} {kern:26s} {'ok' if ok else 'MISMATCH'}", flush=True)
+    assert ok
