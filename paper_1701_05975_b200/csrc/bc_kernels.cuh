@@ -136,6 +136,7 @@ struct RunParams {
   uint32_t l2hot;          // device ids < l2hot get evict-last L2 hints
   unsigned long long* prof;  // null or kProfCounters per-run work counters
   const unsigned long long* k_dev;  // if set, the source count is read here (device-side)
+  uint32_t team_base;               // first workspace slot of this launch (fill launches)
 };
 
 // Work counters (accumulated per source when RunParams::prof is set).

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
     ring = cl.map_shared_rank(sh.ring, 0);
   }
   const bool leader = rank == 0 && tid == 0;
-  const uint32_t team = blockIdx.x / C;
+  const uint32_t team = p.team_base + blockIdx.x / C;
   const uint64_t off = static_cast<uint64_t>(team) * p.ws.n_stride;
   const uint64_t keep_pol = l2_policy_evict_last();
   const uint64_t stream_pol = l2_policy_evict_first();

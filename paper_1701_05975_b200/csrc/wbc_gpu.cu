@@ -115,6 +115,10 @@ struct wbc_gpu_graph {
   wbc_dev::Workspace ws_fb{};
   int fb_slots = 0;
   bool last_warp = false;     // the last run used bc_warp_kernel (layout wl / ws_fb)
+  int fill = 0;               // 2-CTA fill clusters beside a C >= 4 team launch
+  int tune_fill = 0;          // opt-in: measured slower (R-MAT-24 C=16: 31.3 vs 32.5 GTEPS)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint32_t* d_abort_list = nullptr;
   uint64_t abort_cap = 0;
   unsigned long long* d_abort_count = nullptr;
@@ -145,6 +149,9 @@ struct wbc_gpu_graph {
 
   ~wbc_gpu_graph() {
     cudaSetDevice(device);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     for (void* p : {(void*)d_offsets, (void*)d_slots32, (void*)d_slots64, (void*)d_minw,
                     (void*)d_edge_id, (void*)d_perm, (void*)d_inv, d_ws, (void*)d_counter,
                     (void*)d_abort_list, (void*)d_abort_count, (void*)d_counter2,
@@ -245,10 +252,10 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
     s.cluster = c;
     s.threads = 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
-    // near window: flat optimum around 8-16 on skewed graphs (R-MAT-20 45.2
-    // GTEPS at 8 vs 44.6 at the automatic 18; BA 30.4 at 8 vs 28.7 at 2;
-    // R-MAT-24 33.8 at 8 vs 32.9 at 19)
-    if (!g->tune_near) s.near_width = std::min<uint32_t>(16, std::max<uint32_t>(8, g->near_width));
+    // near window: 8 was the measured optimum on every skewed config (R-MAT-20
+    // 45.2 GTEPS at 8 vs 44.6 at the automatic 18; BA 30.4 at 8 vs 28.7 at 2;
+    // R-MAT-24 33.8 at 8 vs 32.9 at 19; weights up to 255)
+    if (!g->tune_near) s.near_width = 8;
     return s;
   }
   // Flat, large graphs (grid / road-like: latency-bound rounds, small
@@ -437,13 +444,28 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   }
   if (g->tune_slots) slots = std::min(slots, g->tune_slots);
   slots = std::max(1, std::min(slots, want));
+  // Clusters of 4..16 CTAs strand the SMs no such cluster fits on (7 x 16
+  // CTAs leave 36 of 148 SMs idle): a concurrent launch of 2-CTA clusters
+  // fills them, sharing the source counter.
+  int fill = 0;
+  if (team && !shape.warp && shape.cluster >= 4 && g->tune_fill && want > slots) {
+    fill = std::max(0, (g->sm_count - slots * shape.cluster) / 2);
+    fill = std::min<int>(fill, want - slots);
+    if (fill > 0)
+      for (const bool prof : {false, true})
+        WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(2, shape.threads, g->packed, prof)),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(shape.dyn_smem)));
+  }
   size_t free_b = 0, total_b = 0;
   WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   uint64_t avail = free_b + (g->d_ws ? g->ws_bytes : 0);
   const uint64_t reserve = (4ULL << 30) + total_b / 10;  // 4 GiB + 10% headroom
   avail = avail > reserve ? avail - reserve : 0;
   slots = static_cast<int>(std::min<uint64_t>(slots, std::max<uint64_t>(1, avail / per_slot)));
-  int rc = ensure_bytes(g, per_slot * slots);
+  fill = static_cast<int>(std::min<uint64_t>(fill, avail / per_slot - std::min<uint64_t>(avail / per_slot, slots)));
+  g->fill = fill;
+  int rc = ensure_bytes(g, per_slot * (slots + fill));
   if (rc) return rc;
   *slots_out = slots;
   char* base = static_cast<char*>(g->d_ws);
@@ -462,7 +484,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     g->ws_team = false;
     return WBC_OK;
   }
-  g->ws = carve_cta_team(g, base, slots, team, one_warp);
+  g->ws = carve_cta_team(g, base, slots + fill, team, one_warp);
   g->ws_slots = slots;
   g->ws_team = team;
   return WBC_OK;
@@ -576,7 +598,28 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = shape.cluster > 1 ? 1 : 0;
+    const int fill = single_slot ? 0 : g->fill;
+    if (fill > 0) {  // fork: the fill launch runs beside the main one on a side stream
+      if (!g->side) {
+        WBC_CUDA_TRY(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        WBC_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+        WBC_CUDA_TRY(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+      }
+      WBC_CUDA_TRY(cudaEventRecord(g->ev_fork, stream));
+      WBC_CUDA_TRY(cudaStreamWaitEvent(g->side, g->ev_fork, 0));
+    }
     WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(shape.cluster, shape.threads, g->packed, g->profiling), p));
+    if (fill > 0) {
+      wbc_dev::RunParams pf = p;
+      pf.team_base = static_cast<uint32_t>(slots);
+      attr[0].val.clusterDim.x = 2;
+      cfg.gridDim = dim3(fill * 2, 1, 1);
+      cfg.numAttrs = 1;
+      cfg.stream = g->side;
+      WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(2, shape.threads, g->packed, g->profiling), pf));
+      WBC_CUDA_TRY(cudaEventRecord(g->ev_join, g->side));
+      WBC_CUDA_TRY(cudaStreamWaitEvent(stream, g->ev_join, 0));  // join
+    }
   } else {
     pick_kernel(shape.threads, g->packed, g->profiling)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p);
     WBC_CUDA_TRY(cudaGetLastError());
@@ -589,7 +632,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  g->stats[3] = shape.warp ? 3 : 2;
+  g->stats[3] = shape.warp ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
   return WBC_OK;
 }
 
@@ -838,6 +881,7 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "l2hot") g->tune_l2hot = value;
   else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
   else if (k == "warp") g->tune_warp = static_cast<int>(value);
+  else if (k == "fill") g->tune_fill = static_cast<int>(value);
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }
