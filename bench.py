@@ -46,7 +46,33 @@ WORKLOADS = {
 
 
 # The reference's fastest bc_parallel schedule per family.
-BEST_STRATEGY = {"er": "np", "ba": "we-warp32", "rmat": "we", "grid": "we"}
+# On the grid bc_parallel is infeasible (O(n * depth) threshold/settle scans:
+# ~17 min per source per thread), so the reference CPU arm there
+# is brandes_sequential (the paper's binary-heap baseline) run as one call per
+# host core over disjoint source shards (SURVEY.md §8(d) i).
+BEST_STRATEGY = {"er": "np", "ba": "we-warp32", "rmat": "we", "grid": "brandes_sequential x cores"}
+
+
+def ref_label(kind, cores):
+    if kind == "grid":
+        return f"brandes_sequential on {cores} threads over disjoint source shards"
+    return f"bc_parallel strategy={BEST_STRATEGY[kind]} workers={cores}"
+
+
+def ref_runner(R, g, kind, cores):
+    """The reference's CPU BC over a source list with all host cores."""
+    if kind != "grid":
+        strategy = BEST_STRATEGY[kind]
+        return lambda src: R.bc_parallel(g, strategy, cores, sources=src)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(src):
+        shards = [s for s in np.array_split(np.asarray(src, np.uint32), cores) if len(s)]
+        with ThreadPoolExecutor(len(shards)) as ex:  # ctypes releases the GIL
+            parts = list(ex.map(lambda sh: R.brandes(g, sources=sh), shards))
+        return np.sum(parts, axis=0)
+    return run
 
 
 def describe(wl: dict) -> str:
@@ -123,6 +149,16 @@ class ClockSampler:
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        # a timed region shorter than the 200 ms poll: keep polling until two
+        # samples exist (at most ~1 s past the region) and say so
+        self.short = False
+        for _ in range(10):
+            self.tmp.flush()
+            with open(self.tmp.name) as f:
+                if len(f.read().splitlines()) >= 2:
+                    break
+            self.short = True
+            time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -145,8 +181,11 @@ class ClockSampler:
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         os.unlink(self.tmp.name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if self.short:
+            out["note"] = "timed region shorter than the 200 ms poll: samples taken at its end"
+        return out
 
 
 def cpu_baseline(wl_name: str, wl: dict, target_s: float = 15.0):
@@ -158,10 +197,11 @@ def cpu_baseline(wl_name: str, wl: dict, target_s: float = 15.0):
         g, src_all = build_graph_ref(R, wl)
         kind = "reference"
         strategy = BEST_STRATEGY[wl["kind"]]
+        ref_step = ref_runner(R, g, wl["kind"], cores)
 
         def run(src):
             t = time.perf_counter()
-            R.bc_parallel(g, strategy, cores, sources=src)
+            ref_step(src)
             return time.perf_counter() - t
     else:  # port: the plain-C oracle, single-threaded
         import paper_1701_05975_b200 as W  # graph arrays only; the timed code is the oracle
@@ -187,8 +227,8 @@ def cpu_baseline(wl_name: str, wl: dict, target_s: float = 15.0):
     if kind == "reference":
         R.free_csr(g)
     return dict(value=value, unit="GTEPS", cores=cores, kind=kind,
-                sample=f"first {len(sample)} of the {wl_name} source list, bc_parallel strategy={strategy} "
-                       f"workers={cores}, {t:.2f}s wall" if kind == "reference" else
+                sample=f"first {len(sample)} of the {wl_name} source list, {ref_label(wl['kind'], cores)}, "
+                       f"{t:.2f}s wall" if kind == "reference" else
                        f"first {len(sample)} sources, oracle bc_eq4 single-thread, {t:.2f}s")
 
 
@@ -219,8 +259,7 @@ def run_reference_arm(args, wl_name, wl):
         R = RefLib()
         g, src_all = build_graph_ref(R, wl)
         kind = "reference"
-        strategy = BEST_STRATEGY[wl["kind"]]
-        step = lambda src: R.bc_parallel(g, strategy, cores, sources=src)  # noqa: E731
+        step = ref_runner(R, g, wl["kind"], cores)
     else:
         _, g, src_all = build_graph_ours(wl)
         O = Oracle()
@@ -249,8 +288,7 @@ def run_reference_arm(args, wl_name, wl):
                             sources_per_step=int(len(sample)),
                             note="bounded sample of the workload's source list per step"),
                 cpu_baseline=dict(value=value, unit="GTEPS", cores=cores, kind=kind,
-                                  sample=f"{len(sample)} sources per step, bc_parallel strategy="
-                                         f"{BEST_STRATEGY[wl['kind']]} workers={cores}"),
+                                  sample=f"{len(sample)} sources per step, {ref_label(wl['kind'], cores)}"),
                 e2e=dict(value=value, unit="GTEPS", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
     return 0

@@ -94,6 +94,7 @@ struct wbc_gpu_graph {
   int smem_per_sm = 0;
   int smem_optin = 0;
   double hot_coverage_25k = 0;  // share of neighbour accesses landing on the top 25K ids
+  bool skewed = false;          // heavy-tailed degrees: max degree >= 16 x average
   // device CSR replica (relabelled ids)
   uint32_t* d_offsets = nullptr;
   uint32_t* d_slots32 = nullptr;
@@ -242,7 +243,7 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   // the per-CTA kernel), else the smallest C in {2,4,8,16} with
   // (148/C) * 4n <= 256 MB (R-MAT-20: C=2, 43 GTEPS; R-MAT-24: C=16, 32.8
   // vs 21.8 at C=2).  Measured on B200, DESIGN.md §4.
-  if (g->tune_cluster < 0 && !tiny && g->hot_coverage_25k >= 0.4) {
+  if (g->tune_cluster < 0 && !tiny && g->skewed) {
     const uint64_t per = n * 4;
     int c = 1;
     if (per * static_cast<uint64_t>(g->sm_count) > (64ULL << 20)) {
@@ -753,6 +754,8 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
     uint64_t top = 0;
     for (uint32_t i = 0; i < std::min<uint32_t>(n, 25 * 1024); ++i) top += noff[i + 1] - noff[i];
     g->hot_coverage_25k = static_cast<double>(top) / static_cast<double>(slots);
+    const double avg = static_cast<double>(slots) / n;
+    g->skewed = static_cast<double>(noff[1] - noff[0]) >= 16.0 * avg;  // perm[0] has the max degree
   }
   std::vector<uint32_t> slot32(g->packed ? slots : 0);
   std::vector<uint2> slot64(g->packed ? 0 : slots);
