@@ -83,6 +83,16 @@ namespace wbc_host {
 int set_error(int code, const std::string& msg) { return ::set_error(code, msg); }
 }  // namespace wbc_host
 
+struct LaunchShape {
+  uint32_t near_width = 0; // 0: the graph's automatic width
+  bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
+  int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
+  int threads = 128;
+  uint32_t hot = 0;        // vertices with shared-memory distances
+  uint32_t l2hot = 0;      // vertices whose distance accesses carry an evict-last hint
+  size_t dyn_smem = 0;     // bytes
+};
+
 struct wbc_gpu_graph {
   int device = 0;
   uint32_t n = 0, m = 0;
@@ -117,6 +127,10 @@ struct wbc_gpu_graph {
   int fb_slots = 0;
   bool last_warp = false;     // the last run used bc_warp_kernel (layout wl / ws_fb)
   int fill = 0;               // 2-CTA fill clusters beside a C >= 4 team launch
+  // launch decisions are cached until a tuning knob changes
+  uint64_t tune_gen = 1, shape_gen = 0, ws_gen = 0;
+  LaunchShape shape_cache{};
+  int ws_want = -1, ws_slots_cached = 0;
   int tune_fill = 0;          // opt-in: measured slower (R-MAT-24 C=16: 31.3 vs 32.5 GTEPS)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -198,15 +212,6 @@ KernelFn pick_team(int c, int threads, bool packed, bool prof = false) {
   return prof ? pick_team_t<false, true>(c, threads) : pick_team_t<false, false>(c, threads);
 }
 
-struct LaunchShape {
-  uint32_t near_width = 0; // 0: the graph's automatic width
-  bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
-  int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
-  int threads = 128;
-  uint32_t hot = 0;        // vertices with shared-memory distances
-  uint32_t l2hot = 0;      // vertices whose distance accesses carry an evict-last hint
-  size_t dyn_smem = 0;     // bytes
-};
 
 // Launch shape policy:
 //  * small graphs (n*4 <= 24 KB): every distance in shared memory, 128-thread
@@ -218,7 +223,11 @@ struct LaunchShape {
 // Unless tuned, the shared-memory distance cache gets exactly the shared
 // memory left over at the register-limited occupancy, so it never costs
 // resident sources.
-LaunchShape pick_shape(const wbc_gpu_graph* g) {
+LaunchShape pick_shape_uncached(const wbc_gpu_graph* g);
+
+LaunchShape pick_shape(wbc_gpu_graph* g);
+
+LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   LaunchShape s;
   const uint64_t n = g->n;
   const bool tiny = n * 4 <= 24 * 1024;
@@ -296,6 +305,14 @@ LaunchShape pick_shape(const wbc_gpu_graph* g) {
   s.hot = static_cast<uint32_t>(hot);
   s.dyn_smem = hot * 4;
   return s;
+}
+
+LaunchShape pick_shape(wbc_gpu_graph* g) {
+  if (g->shape_gen != g->tune_gen) {
+    g->shape_cache = pick_shape_uncached(g);
+    g->shape_gen = g->tune_gen;
+  }
+  return g->shape_cache;
 }
 
 // Per-slot workspace bytes of each kernel family.
@@ -380,6 +397,12 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
+  // same knobs, same request, layout still carved: nothing to query or carve
+  if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want) {
+    *slots_out = g->ws_slots_cached;
+    return WBC_OK;
+  }
+  g->ws_gen = 0;
   const bool team = shape.cluster > 0;
   const bool one_warp = team && shape.cluster == 1 && shape.threads <= 32;
   const uint64_t per_slot = ws_per_slot(g, shape.warp, team, one_warp);
@@ -483,11 +506,14 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
     g->ws_slots = slots;
     g->ws_team = false;
-    return WBC_OK;
+  } else {
+    g->ws = carve_cta_team(g, base, slots + fill, team, one_warp);
+    g->ws_slots = slots;
+    g->ws_team = team;
   }
-  g->ws = carve_cta_team(g, base, slots + fill, team, one_warp);
-  g->ws_slots = slots;
-  g->ws_team = team;
+  g->ws_gen = g->tune_gen;
+  g->ws_want = want;
+  g->ws_slots_cached = slots;
   return WBC_OK;
 }
 
@@ -861,6 +887,7 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uin
                        int64_t hot_vertices) {
   if (!g) return set_error(WBC_E_INVALID, "null graph");
   if (threads_per_cta < 0 || max_slots < 0) return set_error(WBC_E_INVALID, "negative tuning value");
+  ++g->tune_gen;
   g->tune_threads = threads_per_cta;
   g->tune_slots = max_slots;
   g->tune_hot = hot_vertices;
@@ -873,6 +900,7 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots, uin
 
 int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   if (!g || !name) return set_error(WBC_E_INVALID, "null argument");
+  ++g->tune_gen;
   const std::string k = name;
   if (k == "threads") g->tune_threads = static_cast<int>(value);
   else if (k == "slots") g->tune_slots = static_cast<int>(value);
