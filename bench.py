@@ -42,6 +42,8 @@ WORKLOADS = {
     "rmat20": dict(kind="rmat", scale=20, deg=32.0, lo=1, hi=255, sources=4096),
     "grid2048": dict(kind="grid", side=2048, lo=1, hi=1000, sources=1024),
     "rmat24": dict(kind="rmat", scale=24, deg=32.0, lo=1, hi=255, sources=65536),
+    # small test workload (multi-rank checks), not a BASELINE config
+    "rmat16": dict(kind="rmat", scale=16, deg=32.0, lo=1, hi=255, sources=512),
 }
 
 
@@ -306,6 +308,9 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--near", type=int, default=0)
+    ap.add_argument("--dump-bc", default="", help="rank 0 saves the reduced node BC (np.save) here")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share a GPU (multi-rank checks on a one-GPU box)")
     args = ap.parse_args()
     wl = dict(WORKLOADS[args.workload])
     if args.sources:
@@ -321,14 +326,27 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+
+    def all_reduce(t, op=dist.ReduceOp.SUM):
+        """The run's one collective (NCCL on device; gloo via host)."""
+        if args.dist_backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:
+            c = t.cpu()
+            dist.all_reduce(c, op=op)
+            t.copy_(c)
 
     t_build = time.perf_counter()
     _, g, src_all = build_graph_ours(wl)
     t_build = time.perf_counter() - t_build
-    gg = W.GpuGraph(g, device=local)
+    gg = W.GpuGraph(g, device=dev)
     gg.set_tuning(args.threads, args.slots, args.near)
     shard = np.ascontiguousarray(src_all[rank::world])
     n, m = g.n, g.m
@@ -346,7 +364,7 @@ def main():
         if events is not None:
             events[1].record(stream)
         if world > 1:
-            dist.all_reduce(d_node)
+            all_reduce(d_node)
 
     def barrier():
         if world > 1:
@@ -357,7 +375,7 @@ def main():
         device_step()
     barrier()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev)
     clocks.start()
     launch_events = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(args.steps)]
@@ -375,11 +393,13 @@ def main():
     kernel_s = [a.elapsed_time(b) / 1e3 for a, b in launch_events]
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     total_sources = len(src_all)
     value = m * total_sources * args.steps / elapsed / 1e9
     bc_sum = float(d_node.sum().item())
+    if args.dump_bc and rank == 0:
+        np.save(args.dump_bc, d_node.cpu().numpy())
 
     # ---- e2e through the host-buffer C ABI (wbc_gpu_bc): H2D sources, D2H results
     opt = W.EngineOptions(sources=shard)
@@ -393,13 +413,13 @@ def main():
         host_node = r.node_bc
         if world > 1:
             tt = torch.from_numpy(host_node).cuda()
-            dist.all_reduce(tt)
+            all_reduce(tt)
             host_node = tt.cpu().numpy()
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = m * total_sources * args.steps / e2e_s / 1e9
     h2d = 4 * len(shard) + (8 * n if world > 1 else 0)
@@ -425,6 +445,7 @@ def main():
                     scaling="strong", vs_baseline=None, dtype="u32 dist / f64 sigma,delta,BC", data="synthetic",
                     config=dict(workload=args.workload, graph=describe(wl), n=int(n), m=int(m),
                                 sources_per_step=int(total_sources), parallelism=f"source-partitioned x{world}",
+                                collective="none" if world == 1 else f"one {args.dist_backend} all_reduce of the partial BC",
                                 l2="inputs exceed L2 (CSR replica + per-source workspaces >> 126 MB), no flush",
                                 graph_build_s=round(t_build, 2)),
                     e2e=dict(value=round(e2e_value, 3), unit="GTEPS", h2d_bytes_per_step=int(h2d),
