@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libwbc_b200.so")
+# WBC_LIB overrides the library path (A/B experiments between builds)
+LIB_PATH = os.environ.get("WBC_LIB") or os.path.join(HERE, "lib", "libwbc_b200.so")
 
 WBC_OK = 0
 WBC_E_INVALID = -1
