@@ -42,7 +42,7 @@ namespace wbc_dev {
 namespace cg = cooperative_groups;
 
 constexpr uint32_t kInfDist = 0xFFFFFFFFu;
-constexpr int kUnroll = 3;  // independent edge chains per lane in relax (4: 43.9, 3: 44.6 GTEPS on R-MAT-20; 6 and 8 spill and thrash L1)
+constexpr int kUnroll = 2;  // 32-edge groups per warp step in relax (R-MAT-20: 1: 38.2, 2: 44.8, 3: 44.4, 4: 43.9, 6: 32.3, 8: 17.3 GTEPS)
 
 // ---- L2 residency hints.  The CSR slot stream (read once per source, 4 B
 // per slot, far larger than L2) is marked evict-first and skips L1; the
