@@ -21,6 +21,8 @@
 //    (a hub row may be split between CTAs; the sums are integer-valued, hence
 //    exact in any order), and the relax issues the atomicMin, min-weight and
 //    sigma accesses of all its unrolled groups before consuming any of them;
+//    a DAG record holds the predecessor itself (the slot only when edge BC
+//    needs edge_id), so the backward sweep gathers no CSR slot;
 //    queue appends are ballot-aggregated, one atomic per queue per warp step;
 //  * the near/far queues are ping-pong buffers (in-place compaction across
 //    warps would race; one-warp teams get the same buffer twice, which is
@@ -354,10 +356,10 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
               auto drain_pred = [&](uint32_t m) {
                 const uint32_t i = pq_n - m + lane;
                 const bool act = lane < m;
-                uint32_t v = 0, sl = 0;
+                uint32_t u = 0, v = 0, sl = 0;
                 double sg = 0.0;
                 if (act) {
-                  const uint32_t u = qpu[i];
+                  u = qpu[i];
                   v = qpv[i];
                   sl = qps[i];
                   sg = __ldcg(sigma + u);
@@ -367,8 +369,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
                 base = dag_len + __shfl_sync(0xffffffffu, base, 0);
                 if (act) {
                   atomicAdd(sigma + v, sg);
+                  // (predecessor, v); (slot of v's row, v) when edge BC needs edge_id
                   if (base + lane < dag_cap)
-                    dag[base + lane] = make_uint2(sl, v);
+                    dag[base + lane] = make_uint2(p.edge_bc ? sl : u, v);
                   else
                     over = true;
                 }
@@ -666,8 +669,8 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
 #pragma unroll
           for (int k = 0; k < kBackU; ++k) {
             uint32_t w;
-            u[k] = 0;
-            if (c + k * TT < e) load_slot<PACKED>(g, d[k].x, u[k], w);
+            u[k] = d[k].x;  // the predecessor itself unless edge BC stored the slot
+            if (p.edge_bc && c + k * TT < e) load_slot<PACKED>(g, d[k].x, u[k], w);
           }
 #pragma unroll
           for (int k = 0; k < kBackU; ++k) {

@@ -679,13 +679,15 @@ struct Slot0 {
 
 int slot0_state(wbc_gpu_graph* g, Slot0* out) {
   const wbc_dev::Workspace& w = g->ws;
-  *out = Slot0{w.dist, w.sigma, w.delta, w.order, w.level_ends, w.dag_ends, w.dag, false, false};
+  // team-kernel DAG records hold the predecessor (single-source runs never
+  // compute edge BC); the per-CTA kernel records the slot
+  *out = Slot0{w.dist, w.sigma, w.delta, w.order, w.level_ends, w.dag_ends, w.dag, g->ws_team, false};
   if (!g->last_warp) return WBC_OK;
   unsigned long long aborted = 0;
   WBC_CUDA_TRY(cudaMemcpy(&aborted, g->d_abort_count, 8, cudaMemcpyDeviceToHost));
   if (aborted) {
     const wbc_dev::Workspace& f = g->ws_fb;
-    *out = Slot0{f.dist, f.sigma, f.delta, f.order, f.level_ends, f.dag_ends, f.dag, false, false};
+    *out = Slot0{f.dist, f.sigma, f.delta, f.order, f.level_ends, f.dag_ends, f.dag, true, false};
   } else {
     const wbc_dev::WarpParams& l = g->wl;
     *out = Slot0{l.dist, l.sigma, l.delta, l.order, l.level_ends, l.dag_ends, l.dag, true, true};
