@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
 #pragma unroll
                 for (int k = 0; k < kUnroll; ++k) {
                   const uint32_t eg = e0 + 32 * k;
-                  jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0) : 0;
+                  jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0, g.long_rows) : 0;
                   const uint32_t e = eg + lane;
                   slot[k] = e < we ? sh.rowadj[jj[k]] + e : 0xFFFFFFFFu;
                 }

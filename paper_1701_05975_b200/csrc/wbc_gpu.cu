@@ -542,6 +542,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   p.g.edge_id = g->d_edge_id;
   p.g.wbits = g->wbits;
   p.g.wmask = g->wbits >= 32 ? 0xFFFFFFFFu : ((1u << g->wbits) - 1);
+  p.g.long_rows = g->n && 2ULL * g->m >= 32ULL * g->n;
   p.ws = g->ws;
   p.sources = d_sources;
   p.k = k;
