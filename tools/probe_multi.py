@@ -9,7 +9,7 @@ ap.add_argument("--k", type=int, default=296)
 ap.add_argument("--clusters", default="2,4,8")
 ap.add_argument("--nears", default="0")
 ap.add_argument("--l2hots", default="-1")
-ap.add_argument("--mids", default="16")
+ap.add_argument("--mids", default="")
 a = ap.parse_args()
 t = time.time()
 if a.graph.startswith("grid"):
@@ -30,8 +30,10 @@ t = time.time(); gg = W.GpuGraph(g, 0); print(f"upload {time.time()-t:.1f}s {gg.
 src = W.sample_sources(g.n, a.k, 1)
 import itertools
 default_near = gg.info()["near_width"]
-for c, nw, lh, md in itertools.product(a.clusters.split(","), a.nears.split(","), a.l2hots.split(","), a.mids.split(",")):
-    gg.set_param("mid", int(md))
+for c, nw, lh, md in itertools.product(a.clusters.split(","), a.nears.split(","), a.l2hots.split(","),
+                                     a.mids.split(",") if a.mids else ["-"]):
+    if md != "-":
+        gg.set_param("mid", int(md))
     gg.set_param("cluster", int(c))
     if int(nw) > 0:
         gg.set_param("near_width", int(nw))
