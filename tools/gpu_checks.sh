@@ -11,3 +11,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:bc_t
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool python tools/sanitize_cases.py 2>&1 | tail -3
 done
+for wl in er4096 ba65536 grid2048; do
+  timeout 1200 python bench.py --workload $wl --steps 3 --warmup 3 > gpurun_out/bench_$wl.json
+done
+timeout 1800 python bench.py --workload rmat24 --sources 592 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_rmat24.json
