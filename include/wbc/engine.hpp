@@ -46,13 +46,16 @@ struct EngineOptions {
 
 /// GPU knobs live outside the reference's option struct.
 struct GpuOptions {
-  int device = -1;          // -1: current CUDA device
+  int device = -1;          // >= 0: that device; -1: WBC_GPU_DEVICES ("0,1,..." or "all"),
+                            //   else every visible device (sources sharded, one all-reduce)
   int threads_per_cta = 0;  // 0: automatic
   int max_slots = 0;        // 0: automatic (resident sources per GPU)
 };
 
 /// Drop-in for wbc::bc_parallel (reference engine.cpp:372-457).  Uploads g to
-/// the GPU on each call; use GpuBcEngine to keep the graph resident.
+/// every visible GPU (or WBC_GPU_DEVICES) on each call, shards the sources
+/// across them and combines the partial BC with one NCCL all-reduce; use
+/// GpuBcEngine to keep the graph resident.
 /// settle_rule = LessEqual (a CPU-only negative control) is rejected with
 /// std::invalid_argument.
 BcResult bc_parallel(const CsrGraph& g, const EngineOptions& opt = {});

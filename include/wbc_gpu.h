@@ -179,6 +179,32 @@ void wbc_host_csr_get(const wbc_csr* g, uint32_t* offsets, uint32_t* adjacency,
                       uint64_t* original_id, uint32_t* edge_u, uint32_t* edge_v);
 void wbc_host_csr_free(wbc_csr* g);
 
+/* ---- One process, several GPUs (SURVEY.md §8(b) num_gpus, §8(e)). -------
+ * Replaces: the reference's single-process bc_parallel over all workers
+ * (engine.cpp:372-457), here over several devices: each holds a full CSR
+ * replica, sources are sharded strided across them (sources[i::D]), and the
+ * partial node/edge BC and depth vectors are combined by one NCCL all-reduce
+ * (sum / sum / max) -- NCCL is loaded at run time (the process's own libnccl
+ * if already loaded).  Without NCCL, or when a device repeats in `devices`
+ * (test mode on one-GPU machines), device-to-device copies plus an add kernel
+ * on the first device combine them instead.  Same argument contract and
+ * error behaviour as wbc_gpu_graph_create / wbc_gpu_bc. */
+typedef struct wbc_gpu_multi wbc_gpu_multi;
+#define WBC_MULTI_NO_NCCL 1     /* combine with device copies even if NCCL is available */
+#define WBC_MULTI_FORCE_NCCL 2  /* use NCCL even for a single device (tests) */
+int wbc_gpu_device_count(int* count);
+int wbc_gpu_multi_create(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
+                         const double* weights, const double* min_incident_weight,
+                         const uint32_t* edge_id, const int* devices, int num_devices, int flags,
+                         wbc_gpu_multi** out);
+int wbc_gpu_multi_bc(wbc_gpu_multi* h, const uint32_t* sources, uint64_t k, uint32_t flags,
+                     double* node_bc, double* edge_bc, uint32_t* depth_per_source,
+                     double* elapsed_s);
+int wbc_gpu_multi_info(wbc_gpu_multi* h, int* num_devices, int* uses_nccl);
+/* The per-device graph handle (tuning knobs, last_run_stats); owned by h. */
+wbc_gpu_graph* wbc_gpu_multi_device_graph(wbc_gpu_multi* h, int i);
+void wbc_gpu_multi_destroy(wbc_gpu_multi* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import io
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -32,7 +33,8 @@ __all__ = [
     "ParseError", "EdgeList", "CsrGraph", "GraphStats", "parse_edge_list", "build_csr", "graph_stats",
     "to_edge_list", "write_edge_list", "gen_er", "gen_kronecker", "gen_ba", "gen_grid", "assign_weights",
     "sample_sources", "FrontierMode", "Strategy", "valid_lane_width", "strategy_name", "parse_strategy",
-    "SettleRule", "Normalization", "EngineOptions", "BcResult", "GpuGraph", "bc_parallel", "kInf",
+    "SettleRule", "Normalization", "EngineOptions", "BcResult", "GpuGraph", "MultiGpuGraph", "device_count",
+    "resolve_devices", "bc_parallel", "kInf",
 ]
 
 kInf = float("inf")
@@ -320,21 +322,48 @@ def _validate(opt: EngineOptions) -> None:
         raise ValueError("bc_parallel: SettleRule::LessEqual is a CPU-only negative control (not run on GPU)")
 
 
+def _run_bc(fn, h, n: int, m: int, opt: Optional[EngineOptions]) -> BcResult:
+    """Shared argument handling of wbc_gpu_bc / wbc_gpu_multi_bc (engine.cpp:372-457)."""
+    opt = opt or EngineOptions()
+    _validate(opt)
+    node = np.zeros(n, np.float64)
+    edge = np.zeros(m if opt.compute_edge_bc else 0, np.float64)
+    depth = np.zeros(n, np.uint32)
+    if opt.sources is not None:
+        src = np.ascontiguousarray(np.asarray(opt.sources, dtype=np.int64))
+        if len(src) and (src.min() < 0 or src.max() >= n):
+            raise ValueError("bc_parallel: source id out of range")
+        src = src.astype(np.uint32)
+        if len(src) == 0:
+            return BcResult(node, edge, depth, 0.0)
+    else:
+        src = None
+    flags = (L.WBC_HALVED if opt.normalization == Normalization.Halved else 0) | \
+            (L.WBC_EDGE_BC if opt.compute_edge_bc else 0)
+    el = C.c_double()
+    rc = fn(h, _p(src), 0 if src is None else len(src), flags, _p(node),
+            _p(edge) if opt.compute_edge_bc else None, _p(depth), C.byref(el))
+    if rc:
+        _raise(rc)
+    return BcResult(node, edge, depth, el.value)
+
+
+def _csr_arrays(g: CsrGraph):
+    return [np.ascontiguousarray(g.offsets, np.uint32), np.ascontiguousarray(g.adjacency, np.uint32),
+            np.ascontiguousarray(g.weights, np.float64), np.ascontiguousarray(g.min_incident_weight, np.float64),
+            np.ascontiguousarray(g.edge_id, np.uint32)]
+
+
 class GpuGraph:
     """A CsrGraph resident on one GPU (wbc_gpu_graph_create); reuse across runs."""
 
     def __init__(self, g: CsrGraph, device: int = -1):
         lib = L.load()
         self.n, self.m = int(g.n), int(g.m)
-        self._keep = [np.ascontiguousarray(g.offsets, np.uint32), np.ascontiguousarray(g.adjacency, np.uint32),
-                      np.ascontiguousarray(g.weights, np.float64),
-                      np.ascontiguousarray(g.min_incident_weight, np.float64),
-                      np.ascontiguousarray(g.edge_id, np.uint32)]
-        off, adj, w, mw, eid = self._keep
+        off, adj, w, mw, eid = _csr_arrays(g)
         h = C.c_void_p()
         rc = lib.wbc_gpu_graph_create(self.n, self.m, _p(off), _p(adj), _p(w), _p(mw),
                                       _p(eid) if len(eid) == len(adj) else None, device, C.byref(h))
-        self._keep = None
         if rc:
             _raise(rc)
         self._h = h
@@ -398,29 +427,7 @@ class GpuGraph:
 
     def bc(self, opt: Optional[EngineOptions] = None) -> BcResult:
         """bc_parallel semantics on the resident graph (engine.cpp:372-457)."""
-        opt = opt or EngineOptions()
-        _validate(opt)
-        n, m = self.n, self.m
-        node = np.zeros(n, np.float64)
-        edge = np.zeros(m if opt.compute_edge_bc else 0, np.float64)
-        depth = np.zeros(n, np.uint32)
-        if opt.sources is not None:
-            src = np.ascontiguousarray(np.asarray(opt.sources, dtype=np.int64))
-            if len(src) and (src.min() < 0 or src.max() >= n):
-                raise ValueError("bc_parallel: source id out of range")
-            src = src.astype(np.uint32)
-            if len(src) == 0:
-                return BcResult(node, edge, depth, 0.0)
-        else:
-            src = None
-        flags = (L.WBC_HALVED if opt.normalization == Normalization.Halved else 0) | \
-                (L.WBC_EDGE_BC if opt.compute_edge_bc else 0)
-        el = C.c_double()
-        rc = L.load().wbc_gpu_bc(self._h, _p(src), 0 if src is None else len(src), flags, _p(node),
-                                 _p(edge) if opt.compute_edge_bc else None, _p(depth), C.byref(el))
-        if rc:
-            _raise(rc)
-        return BcResult(node, edge, depth, el.value)
+        return _run_bc(L.load().wbc_gpu_bc, self._h, self.n, self.m, opt)
 
     def bc_device(self, d_sources_ptr: int, k: int, d_node_ptr: int, d_depth_ptr: int = 0,
                   d_edge_ptr: int = 0, halved: bool = False, edge_bc: bool = False, stream: int = 0) -> None:
@@ -466,6 +473,77 @@ class GpuGraph:
         return [np.sort(order[ends[i]:ends[i + 1]]) for i in range(nl.value)]
 
 
+
+def device_count() -> int:
+    """Visible CUDA devices (wbc_gpu_device_count); 0 without a GPU."""
+    c = C.c_int()
+    return c.value if L.load().wbc_gpu_device_count(C.byref(c)) == 0 else 0
+
+
+def resolve_devices(device: int = -1) -> list:
+    """Devices bc_parallel runs on: `device` if >= 0, else WBC_GPU_DEVICES
+    ("0,1,..." or "all"), else every visible device (host_engine.cpp resolve_devices)."""
+    if device >= 0:
+        return [device]
+    count = device_count()
+    if count < 1:
+        return [-1]
+    env = os.environ.get("WBC_GPU_DEVICES", "")
+    if env and env != "all":
+        out = [int(t) for t in env.split(",") if t]
+        if out:
+            return out
+    return list(range(count))
+
+
+class MultiGpuGraph:
+    """A CsrGraph replicated on several GPUs (wbc_gpu_multi_create).  bc() shards
+    the sources strided across the devices and combines the partial BC with one
+    NCCL all-reduce, or device copies when NCCL is absent / a device repeats.
+    Results match GpuGraph.bc to fp64 summation order."""
+
+    def __init__(self, g: CsrGraph, devices: Sequence[int], nccl: Optional[bool] = None):
+        lib = L.load()
+        self.n, self.m = int(g.n), int(g.m)
+        off, adj, w, mw, eid = _csr_arrays(g)
+        devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+        flags = 0 if nccl is None else (L.WBC_MULTI_FORCE_NCCL if nccl else L.WBC_MULTI_NO_NCCL)
+        h = C.c_void_p()
+        rc = lib.wbc_gpu_multi_create(self.n, self.m, _p(off), _p(adj), _p(w), _p(mw),
+                                      _p(eid) if len(eid) == len(adj) else None, _p(devs), len(devs), flags,
+                                      C.byref(h))
+        if rc:
+            _raise(rc)
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.load().wbc_gpu_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        nd, nc = C.c_int(), C.c_int()
+        rc = L.load().wbc_gpu_multi_info(self._h, C.byref(nd), C.byref(nc))
+        if rc:
+            _raise(rc)
+        return dict(num_devices=nd.value, uses_nccl=bool(nc.value))
+
+    def set_param(self, name: str, value: int):
+        lib = L.load()
+        for i in range(self.info()["num_devices"]):
+            rc = lib.wbc_gpu_set_param(lib.wbc_gpu_multi_device_graph(self._h, i), name.encode(), int(value))
+            if rc:
+                _raise(rc)
+
+    def bc(self, opt: Optional[EngineOptions] = None) -> BcResult:
+        return _run_bc(L.load().wbc_gpu_multi_bc, self._h, self.n, self.m, opt)
+
 def bc_parallel(g: CsrGraph, opt: Optional[EngineOptions] = None) -> BcResult:
     """Drop-in for wbc::bc_parallel (engine.hpp:122-130) running on the GPU."""
     opt = opt or EngineOptions()
@@ -478,7 +556,8 @@ def bc_parallel(g: CsrGraph, opt: Optional[EngineOptions] = None) -> BcResult:
         return BcResult(np.zeros(0), np.zeros(0), np.zeros(0, np.uint32), 0.0)
     if opt.sources is not None and len(opt.sources) == 0:
         return BcResult(np.zeros(g.n), np.zeros(g.m if opt.compute_edge_bc else 0), np.zeros(g.n, np.uint32), 0.0)
-    gg = GpuGraph(g)
+    devs = resolve_devices()
+    gg = MultiGpuGraph(g, devs) if len(devs) > 1 else GpuGraph(g, devs[0])
     try:
         return gg.bc(opt)
     finally:

@@ -22,6 +22,8 @@ WBC_E_NOT_BUILT = -5
 WBC_E_PARSE = -6
 WBC_HALVED = 1
 WBC_EDGE_BC = 2
+WBC_MULTI_NO_NCCL = 1
+WBC_MULTI_FORCE_NCCL = 2
 
 vp = C.c_void_p
 u32, u64, i32, i64, f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_int64, C.c_double
@@ -44,6 +46,12 @@ SIGNATURES = [
     ("wbc_gpu_profile_counters", i32, [vp, vp]),
     ("wbc_gpu_last_run_stats", i32, [vp, vp]),
     ("wbc_gpu_last_error", C.c_char_p, []),
+    ("wbc_gpu_device_count", i32, [C.POINTER(i32)]),
+    ("wbc_gpu_multi_create", i32, [u32, u32, vp, vp, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),
+    ("wbc_gpu_multi_bc", i32, [vp, vp, u64, u32, vp, vp, vp, C.POINTER(f64)]),
+    ("wbc_gpu_multi_info", i32, [vp, C.POINTER(i32), C.POINTER(i32)]),
+    ("wbc_gpu_multi_device_graph", vp, [vp, i32]),
+    ("wbc_gpu_multi_destroy", None, [vp]),
     ("wbc_host_parse_edge_list", i32, [C.c_char_p, C.c_size_t, f64, C.POINTER(vp), C.POINTER(u64)]),
     ("wbc_host_edges_new", vp, [u64, vp, vp, vp]),
     ("wbc_host_edges_len", u64, [vp]),

@@ -687,6 +687,20 @@ __global__ void scatter_add_kernel(double* out, const double* in, const uint32_t
     out[perm[i]] += in[i];
 }
 
+// dst += src (partial BC of another device, multi-GPU reduction without NCCL)
+__global__ void add_f64_kernel(double* dst, const double* src, uint64_t len) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] += src[i];
+}
+
+// dst = max(dst, src) (depth_per_source of disjoint source shards)
+__global__ void max_u32_kernel(uint32_t* dst, const uint32_t* src, uint64_t len) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = max(dst[i], src[i]);
+}
+
 __global__ void fill_u32_kernel(uint32_t* x, uint64_t len, uint32_t v) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)

@@ -6,8 +6,11 @@
 // empty source list / empty graph return zeros (engine.cpp:382-385),
 // depth_per_source sized n (engine.cpp:379), Halved (engine.cpp:451-454).
 // The GPU computes the same sums; the CPU schedule fields only validate.
+#include <cstdlib>
+#include <sstream>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "wbc/engine.hpp"
 #include "wbc_gpu.h"
@@ -68,20 +71,61 @@ void validate(const EngineOptions& opt) {
 
 }  // namespace
 
+namespace {
+
+// GpuOptions::device >= 0: that device.  -1: the devices listed in
+// WBC_GPU_DEVICES ("0,1,2" -- repeats allowed, for tests -- or "all"), else
+// every visible device.
+std::vector<int> resolve_devices(int device) {
+  if (device >= 0) return {device};
+  int count = 0;
+  if (wbc_gpu_device_count(&count) || count < 1) return {-1};  // fails loudly at create
+  std::vector<int> out;
+  const char* e = std::getenv("WBC_GPU_DEVICES");
+  if (e && std::string(e) != "all") {
+    std::stringstream ss(e);
+    std::string tok;
+    while (std::getline(ss, tok, ','))
+      if (!tok.empty()) out.push_back(std::stoi(tok));
+  }
+  if (out.empty())
+    for (int d = 0; d < count; ++d) out.push_back(d);
+  return out;
+}
+
+}  // namespace
+
 struct GpuBcEngine::Impl {
-  wbc_gpu_graph* h = nullptr;
-  ~Impl() { wbc_gpu_graph_destroy(h); }
+  wbc_gpu_graph* h = nullptr;   // one device
+  wbc_gpu_multi* mh = nullptr;  // several devices: sources sharded, one all-reduce
+  ~Impl() {
+    if (mh)
+      wbc_gpu_multi_destroy(mh);
+    else
+      wbc_gpu_graph_destroy(h);
+  }
 };
 
 GpuBcEngine::GpuBcEngine(const CsrGraph& g, const GpuOptions& gpu)
     : impl_(std::make_unique<Impl>()), n_(g.n), m_(g.m) {
-  const int rc = wbc_gpu_graph_create(g.n, g.m, g.offsets.data(), g.adjacency.data(),
-                                      g.weights.data(), g.min_incident_weight.data(),
-                                      g.edge_id.empty() ? nullptr : g.edge_id.data(), gpu.device,
-                                      &impl_->h);
-  if (rc) throw_status(rc);
+  const std::vector<int> devs = resolve_devices(gpu.device);
+  const uint32_t* eid = g.edge_id.empty() ? nullptr : g.edge_id.data();
+  int rc;
+  if (devs.size() > 1) {
+    rc = wbc_gpu_multi_create(g.n, g.m, g.offsets.data(), g.adjacency.data(), g.weights.data(),
+                              g.min_incident_weight.data(), eid, devs.data(), static_cast<int>(devs.size()), 0,
+                              &impl_->mh);
+    if (rc) throw_status(rc);
+    impl_->h = wbc_gpu_multi_device_graph(impl_->mh, 0);
+  } else {
+    rc = wbc_gpu_graph_create(g.n, g.m, g.offsets.data(), g.adjacency.data(), g.weights.data(),
+                              g.min_incident_weight.data(), eid, devs[0], &impl_->h);
+    if (rc) throw_status(rc);
+  }
   if (gpu.threads_per_cta || gpu.max_slots)
-    wbc_gpu_set_tuning(impl_->h, gpu.threads_per_cta, gpu.max_slots, 0, -1);
+    for (int i = 0; wbc_gpu_graph* dh = impl_->mh ? wbc_gpu_multi_device_graph(impl_->mh, i) : (i ? nullptr : impl_->h);
+         ++i)
+      wbc_gpu_set_tuning(dh, gpu.threads_per_cta, gpu.max_slots, 0, -1);
 }
 
 GpuBcEngine::~GpuBcEngine() = default;
@@ -103,9 +147,12 @@ BcResult GpuBcEngine::bc(const EngineOptions& opt) const {
     if (k == 0) return r;  // engine.cpp:382-385
   }
   double elapsed = 0.0;
-  const int rc = wbc_gpu_bc(impl_->h, src, k, flags, r.node_bc.data(),
-                            opt.compute_edge_bc ? r.edge_bc.data() : nullptr,
-                            r.depth_per_source.data(), &elapsed);
+  const int rc = impl_->mh ? wbc_gpu_multi_bc(impl_->mh, src, k, flags, r.node_bc.data(),
+                                              opt.compute_edge_bc ? r.edge_bc.data() : nullptr,
+                                              r.depth_per_source.data(), &elapsed)
+                           : wbc_gpu_bc(impl_->h, src, k, flags, r.node_bc.data(),
+                                        opt.compute_edge_bc ? r.edge_bc.data() : nullptr,
+                                        r.depth_per_source.data(), &elapsed);
   if (rc) throw_status(rc);
   r.elapsed = std::chrono::duration<double>(elapsed);
   return r;

@@ -705,16 +705,21 @@ int scale_async(double* x, uint64_t len, double f, cudaStream_t stream) {
 
 }  // namespace
 
-extern "C" {
+namespace {
 
-const char* wbc_gpu_last_error(void) { return g_last_error.c_str(); }
+// Host side of a graph upload, computed once and shared by every device of
+// a multi-GPU handle: validation, degree-descending relabel, packed slots.
+struct HostCsr {
+  uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1;
+  bool packed = true, skewed = false, has_edge_id = false;
+  double hot_coverage_25k = 0;
+  std::vector<uint32_t> perm, inv, noff, slot32, eid, minw;
+  std::vector<uint2> slot64;
+};
 
-int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
-                         const uint32_t* adjacency, const double* weights,
-                         const double* min_incident_weight, const uint32_t* edge_id, int device,
-                         wbc_gpu_graph** out) {
-  if (!out) return set_error(WBC_E_INVALID, "out is null");
-  *out = nullptr;
+int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
+                 const double* weights, const double* min_incident_weight, const uint32_t* edge_id,
+                 HostCsr& h) {
   const uint64_t slots = 2ULL * m;
   if (slots >= (1ULL << 32)) return set_error(WBC_E_UNSUPPORTED, "2m must fit in u32 slots");
   if (n > 0 && (!offsets || !min_incident_weight))
@@ -738,7 +743,82 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
   }
   if (n > 0 && uint64_t{n} * std::max<uint64_t>(maxw, 1) >= 0xFFFFFFFFULL)
     return set_error(WBC_E_UNSUPPORTED, "n * max_weight must stay below 2^32-1");
+  h.n = n;
+  h.m = m;
+  h.has_edge_id = edge_id != nullptr;
+  h.max_weight = static_cast<uint32_t>(maxw);
+  h.wbits = bits_for(std::max<uint64_t>(maxw, 1));
+  const uint32_t nbits = bits_for(n ? n - 1 : 0);
+  h.packed = (h.wbits + nbits) <= 32;
 
+  // ---- degree-descending relabel (ties by id) ---------------------------
+  std::vector<uint32_t>& perm = h.perm;
+  perm.resize(n);
+  std::iota(perm.begin(), perm.end(), 0u);
+  std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
+    return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
+  });
+  std::vector<uint32_t>& inv = h.inv;
+  inv.resize(n);
+  for (uint32_t i = 0; i < n; ++i) inv[perm[i]] = i;
+  std::vector<uint32_t>& noff = h.noff;
+  noff.assign(uint64_t{n} + 1, 0);
+  for (uint32_t i = 0; i < n; ++i) noff[i + 1] = noff[i] + (offsets[perm[i] + 1] - offsets[perm[i]]);
+  if (slots) {
+    uint64_t top = 0;
+    for (uint32_t i = 0; i < std::min<uint32_t>(n, 25 * 1024); ++i) top += noff[i + 1] - noff[i];
+    h.hot_coverage_25k = static_cast<double>(top) / static_cast<double>(slots);
+    const double avg = static_cast<double>(slots) / n;
+    h.skewed = static_cast<double>(noff[1] - noff[0]) >= 16.0 * avg;  // perm[0] has the max degree
+  }
+  h.slot32.assign(h.packed ? slots : 0, 0);
+  h.slot64.assign(h.packed ? 0 : slots, make_uint2(0, 0));
+  h.eid.assign(edge_id ? slots : 0, 0);
+  h.minw.assign(n, 0);
+  double sum_minw = 0;
+  uint64_t cnt_minw = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t v = perm[i];
+    const double x = min_incident_weight[v];
+    if (std::isinf(x) || offsets[v + 1] == offsets[v]) {
+      h.minw[i] = wbc_dev::kInfDist;
+    } else {
+      h.minw[i] = static_cast<uint32_t>(x);
+      sum_minw += x;
+      ++cnt_minw;
+    }
+  }
+  const uint32_t wbits = h.wbits;
+  const bool packed = h.packed;
+  parallel_for(n, [&](uint64_t b, uint64_t e) {
+    std::vector<std::pair<uint32_t, uint32_t>> row;  // (new neighbour, old slot)
+    for (uint64_t i = b; i < e; ++i) {
+      const uint32_t v = perm[i];
+      row.clear();
+      for (uint32_t s = offsets[v]; s < offsets[v + 1]; ++s) row.emplace_back(inv[adjacency[s]], s);
+      std::sort(row.begin(), row.end());
+      uint32_t o = noff[i];
+      for (const auto& [u, s] : row) {
+        const uint32_t w = static_cast<uint32_t>(weights[s]);
+        if (packed)
+          h.slot32[o] = (u << wbits) | w;
+        else
+          h.slot64[o] = make_uint2(u, w);
+        if (edge_id) h.eid[o] = edge_id[s];
+        ++o;
+      }
+    }
+  });
+  // Near-window width: about a third of the mean minimum incident weight balances
+  // near rescans against far refills (DESIGN.md §4).
+  h.near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 3.0 + 0.5)) : 1;
+  return WBC_OK;
+}
+
+// Device side: one replica of a prepared graph on `device`.
+int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
+  const uint32_t n = h.n;
+  const uint64_t slots = 2ULL * h.m;
   auto g = new wbc_gpu_graph();
   int dev = device;
   if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
@@ -762,73 +842,15 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
   }
   if (const char* e = std::getenv("WBC_GPU_CLUSTER")) g->tune_cluster = std::atoi(e);  // tuning default
   g->n = n;
-  g->m = m;
-  g->max_weight = static_cast<uint32_t>(maxw);
-  g->wbits = bits_for(std::max<uint64_t>(maxw, 1));
-  const uint32_t nbits = bits_for(n ? n - 1 : 0);
-  g->packed = (g->wbits + nbits) <= 32;
-
-  // ---- degree-descending relabel (ties by id) ---------------------------
-  std::vector<uint32_t>& perm = g->perm;
-  perm.resize(n);
-  std::iota(perm.begin(), perm.end(), 0u);
-  std::stable_sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) {
-    return offsets[a + 1] - offsets[a] > offsets[b + 1] - offsets[b];
-  });
-  std::vector<uint32_t> inv(n);
-  for (uint32_t i = 0; i < n; ++i) inv[perm[i]] = i;
-  std::vector<uint32_t> noff(uint64_t{n} + 1, 0);
-  for (uint32_t i = 0; i < n; ++i) noff[i + 1] = noff[i] + (offsets[perm[i] + 1] - offsets[perm[i]]);
-  if (slots) {
-    uint64_t top = 0;
-    for (uint32_t i = 0; i < std::min<uint32_t>(n, 25 * 1024); ++i) top += noff[i + 1] - noff[i];
-    g->hot_coverage_25k = static_cast<double>(top) / static_cast<double>(slots);
-    const double avg = static_cast<double>(slots) / n;
-    g->skewed = static_cast<double>(noff[1] - noff[0]) >= 16.0 * avg;  // perm[0] has the max degree
-  }
-  std::vector<uint32_t> slot32(g->packed ? slots : 0);
-  std::vector<uint2> slot64(g->packed ? 0 : slots);
-  std::vector<uint32_t> eid(edge_id ? slots : 0);
-  std::vector<uint32_t> minw(n);
-  double sum_minw = 0;
-  uint64_t cnt_minw = 0;
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t v = perm[i];
-    const double x = min_incident_weight[v];
-    if (std::isinf(x) || offsets[v + 1] == offsets[v]) {
-      minw[i] = wbc_dev::kInfDist;
-    } else {
-      minw[i] = static_cast<uint32_t>(x);
-      sum_minw += x;
-      ++cnt_minw;
-    }
-  }
-  const uint32_t wbits = g->wbits;
-  const bool packed = g->packed;
-  parallel_for(n, [&](uint64_t b, uint64_t e) {
-    std::vector<std::pair<uint32_t, uint32_t>> row;  // (new neighbour, old slot)
-    for (uint64_t i = b; i < e; ++i) {
-      const uint32_t v = perm[i];
-      row.clear();
-      for (uint32_t s = offsets[v]; s < offsets[v + 1]; ++s) row.emplace_back(inv[adjacency[s]], s);
-      std::sort(row.begin(), row.end());
-      uint32_t o = noff[i];
-      for (const auto& [u, s] : row) {
-        const uint32_t w = static_cast<uint32_t>(weights[s]);
-        if (packed)
-          slot32[o] = (u << wbits) | w;
-        else
-          slot64[o] = make_uint2(u, w);
-        if (edge_id) eid[o] = edge_id[s];
-        ++o;
-      }
-    }
-  });
-  // Near-window width: about a third of the mean minimum incident weight balances
-  // near rescans against far refills (DESIGN.md §4).
-  g->near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 3.0 + 0.5))
-                           : 1;
-
+  g->m = h.m;
+  g->max_weight = h.max_weight;
+  g->wbits = h.wbits;
+  g->packed = h.packed;
+  g->perm = h.perm;
+  g->hot_coverage_25k = h.hot_coverage_25k;
+  g->skewed = h.skewed;
+  g->near_width = h.near_width;
+  const bool packed = h.packed;
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
   if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);
   if (err == cudaSuccess) g->d_perm = dev_alloc<uint32_t>(n, err);
@@ -843,33 +865,51 @@ int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
     else
       g->d_slots64 = dev_alloc<uint2>(slots, err);
   }
-  if (err == cudaSuccess && edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
+  if (err == cudaSuccess && h.has_edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_NOMEM, std::string("graph upload: ") + cudaGetErrorString(err));
   }
   if (n) {
-    err = cudaMemcpy(g->d_offsets, noff.data(), (uint64_t{n} + 1) * 4, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMemcpy(g->d_minw, minw.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMemcpy(g->d_perm, perm.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess) err = cudaMemcpy(g->d_inv, inv.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+    err = cudaMemcpy(g->d_offsets, h.noff.data(), (uint64_t{n} + 1) * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_minw, h.minw.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_perm, h.perm.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(g->d_inv, h.inv.data(), uint64_t{n} * 4, cudaMemcpyHostToDevice);
   }
   if (err == cudaSuccess && slots) {
     if (packed)
-      err = cudaMemcpy(g->d_slots32, slot32.data(), slots * 4, cudaMemcpyHostToDevice);
+      err = cudaMemcpy(g->d_slots32, h.slot32.data(), slots * 4, cudaMemcpyHostToDevice);
     else
-      err = cudaMemcpy(g->d_slots64, slot64.data(), slots * 8, cudaMemcpyHostToDevice);
-    if (err == cudaSuccess && edge_id)
-      err = cudaMemcpy(g->d_edge_id, eid.data(), slots * 4, cudaMemcpyHostToDevice);
+      err = cudaMemcpy(g->d_slots64, h.slot64.data(), slots * 8, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess && h.has_edge_id)
+      err = cudaMemcpy(g->d_edge_id, h.eid.data(), slots * 4, cudaMemcpyHostToDevice);
   }
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_CUDA, std::string("graph upload: ") + cudaGetErrorString(err));
   }
   g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 12 + slots * (packed ? 4 : 8) +
-                   (edge_id ? slots * 4 : 0);
+                   (h.has_edge_id ? slots * 4 : 0);
   *out = g;
   return WBC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wbc_gpu_last_error(void) { return g_last_error.c_str(); }
+
+int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
+                         const uint32_t* adjacency, const double* weights,
+                         const double* min_incident_weight, const uint32_t* edge_id, int device,
+                         wbc_gpu_graph** out) {
+  if (!out) return set_error(WBC_E_INVALID, "out is null");
+  *out = nullptr;
+  HostCsr h;
+  const int rc = prepare_host(n, m, offsets, adjacency, weights, min_incident_weight, edge_id, h);
+  if (rc) return rc;
+  return upload_graph(h, device, out);
 }
 
 void wbc_gpu_graph_destroy(wbc_gpu_graph* g) { delete g; }
@@ -1145,6 +1185,258 @@ int wbc_gpu_sssp_levels(wbc_gpu_graph* g, uint32_t source, uint32_t* order, uint
   std::memcpy(level_ends, lev.data(), lev.size() * 4);
   *order_len = len;
   *levels = depth;
+  return WBC_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// One process, several GPUs (SURVEY.md §8(b) num_gpus, §8(e)): sources are
+// sharded strided across the devices, each holding a full CSR replica; the
+// partial node/edge BC and depth vectors are combined by ONE NCCL all-reduce
+// (sum / sum / max).  NCCL is dlopen'ed on first use -- if the process already
+// loaded a libnccl (e.g. torch's), that one is used -- so the library itself
+// has no link-time NCCL dependency.  When NCCL is unavailable or a device
+// repeats (the test mode of one-GPU machines), the partials are combined by
+// device-to-device copies and an add kernel on the first device instead.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) return a;
+    a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(dlsym(h, "ncclCommInitAll"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.CommInitAll && a.AllReduce && a.GroupStart && a.GroupEnd && a.CommDestroy && a.GetErrorString;
+    return a;
+  }();
+  return api;
+}
+
+}  // namespace
+
+struct wbc_gpu_multi {
+  uint32_t n = 0, m = 0;
+  std::vector<wbc_gpu_graph*> g;
+  std::vector<cudaStream_t> st;
+  std::vector<ncclComm_t> comm;
+  bool use_nccl = false;
+  std::vector<double*> d_node, d_edge;
+  std::vector<uint32_t*> d_depth, d_src;
+  std::vector<uint64_t> src_cap;
+  double* d_tmp = nullptr;      // first device: staging for the copy reduction
+  uint32_t* d_tmp32 = nullptr;
+  ~wbc_gpu_multi() {
+    if (use_nccl)
+      for (ncclComm_t c : comm) nccl_api().CommDestroy(c);
+    for (size_t i = 0; i < g.size(); ++i) {
+      if (!g[i]) continue;
+      cudaSetDevice(g[i]->device);
+      cudaFree(d_node[i]);
+      cudaFree(d_edge[i]);
+      cudaFree(d_depth[i]);
+      cudaFree(d_src[i]);
+      if (st[i]) cudaStreamDestroy(st[i]);
+      if (i == 0) {
+        cudaFree(d_tmp);
+        cudaFree(d_tmp32);
+      }
+      delete g[i];
+    }
+  }
+};
+
+extern "C" {
+
+int wbc_gpu_device_count(int* count) {
+  if (!count) return set_error(WBC_E_INVALID, "null argument");
+  *count = 0;
+  if (cudaGetDeviceCount(count) != cudaSuccess) {
+    *count = 0;
+    return set_error(WBC_E_NOT_BUILT, "no CUDA device available");
+  }
+  return WBC_OK;
+}
+
+int wbc_gpu_multi_create(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
+                         const double* weights, const double* min_incident_weight, const uint32_t* edge_id,
+                         const int* devices, int num_devices, int flags, wbc_gpu_multi** out) {
+  if (!out || !devices || num_devices < 1) return set_error(WBC_E_INVALID, "devices / out required");
+  *out = nullptr;
+  HostCsr h;
+  int rc = prepare_host(n, m, offsets, adjacency, weights, min_incident_weight, edge_id, h);
+  if (rc) return rc;
+  auto mh = new wbc_gpu_multi();
+  mh->n = n;
+  mh->m = m;
+  const size_t D = static_cast<size_t>(num_devices);
+  mh->g.assign(D, nullptr);
+  mh->st.assign(D, nullptr);
+  mh->d_node.assign(D, nullptr);
+  mh->d_edge.assign(D, nullptr);
+  mh->d_depth.assign(D, nullptr);
+  mh->d_src.assign(D, nullptr);
+  mh->src_cap.assign(D, 0);
+  for (size_t i = 0; i < D; ++i) {
+    if ((rc = upload_graph(h, devices[i], &mh->g[i]))) {
+      delete mh;
+      return rc;
+    }
+    cudaError_t err = cudaSetDevice(mh->g[i]->device);
+    if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&mh->st[i], cudaStreamNonBlocking);
+    if (err == cudaSuccess) mh->d_node[i] = dev_alloc<double>(n, err);
+    if (err == cudaSuccess) mh->d_depth[i] = dev_alloc<uint32_t>(n, err);
+    if (err == cudaSuccess && edge_id) mh->d_edge[i] = dev_alloc<double>(m, err);
+    if (err == cudaSuccess && i == 0 && D > 1) mh->d_tmp = dev_alloc<double>(std::max(n, m), err);
+    if (err == cudaSuccess && i == 0 && D > 1) mh->d_tmp32 = dev_alloc<uint32_t>(n, err);
+    if (err != cudaSuccess) {
+      delete mh;
+      return set_error(WBC_E_NOMEM, std::string("multi-GPU setup: ") + cudaGetErrorString(err));
+    }
+  }
+  // NCCL for distinct devices (or forced for a single device, to exercise it)
+  std::vector<int> devs(D);
+  for (size_t i = 0; i < D; ++i) devs[i] = mh->g[i]->device;
+  std::vector<int> sorted = devs;
+  std::sort(sorted.begin(), sorted.end());
+  const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+  const bool want_nccl = (flags & WBC_MULTI_NO_NCCL) == 0 && distinct && (D > 1 || (flags & WBC_MULTI_FORCE_NCCL));
+  if (want_nccl && nccl_api().ok) {
+    mh->comm.assign(D, nullptr);
+    if (nccl_api().CommInitAll(mh->comm.data(), static_cast<int>(D), devs.data()) == ncclSuccess)
+      mh->use_nccl = true;
+    else
+      mh->comm.clear();
+  }
+  *out = mh;
+  return WBC_OK;
+}
+
+void wbc_gpu_multi_destroy(wbc_gpu_multi* h) { delete h; }
+
+int wbc_gpu_multi_info(wbc_gpu_multi* h, int* num_devices, int* uses_nccl) {
+  if (!h) return set_error(WBC_E_INVALID, "null handle");
+  if (num_devices) *num_devices = static_cast<int>(h->g.size());
+  if (uses_nccl) *uses_nccl = h->use_nccl ? 1 : 0;
+  return WBC_OK;
+}
+
+wbc_gpu_graph* wbc_gpu_multi_device_graph(wbc_gpu_multi* h, int i) {
+  if (!h || i < 0 || static_cast<size_t>(i) >= h->g.size()) return nullptr;
+  return h->g[i];
+}
+
+int wbc_gpu_multi_bc(wbc_gpu_multi* h, const uint32_t* sources, uint64_t k, uint32_t flags, double* node_bc,
+                     double* edge_bc, uint32_t* depth_per_source, double* elapsed_s) {
+  if (!h) return set_error(WBC_E_INVALID, "null handle");
+  const bool edge = flags & WBC_EDGE_BC;
+  const uint32_t n = h->n, m = h->m;
+  if (!node_bc && n) return set_error(WBC_E_INVALID, "node_bc is required");
+  if (edge && !edge_bc && m) return set_error(WBC_E_INVALID, "edge_bc is required");
+  if (edge && !h->d_edge[0])
+    return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
+  if (sources)  // resolve_sources (engine.cpp:349-361)
+    for (uint64_t i = 0; i < k; ++i)
+      if (sources[i] >= n) return set_error(WBC_E_INVALID, "bc_parallel: source id out of range");
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t D = h->g.size();
+  const uint64_t total = sources ? k : n;
+  // strided shard of the source list per device (sources[i::D])
+  std::vector<std::vector<uint32_t>> shard(D);
+  for (uint64_t i = 0; i < total; ++i) shard[i % D].push_back(sources ? sources[i] : static_cast<uint32_t>(i));
+  for (size_t d = 0; d < D; ++d) {
+    wbc_gpu_graph* g = h->g[d];
+    WBC_CUDA_TRY(cudaSetDevice(g->device));
+    const cudaStream_t st = h->st[d];
+    const uint64_t kd = shard[d].size();
+    if (kd > h->src_cap[d]) {
+      cudaFree(h->d_src[d]);
+      cudaError_t err = cudaSuccess;
+      h->d_src[d] = dev_alloc<uint32_t>(kd, err);
+      if (err != cudaSuccess) return set_error(WBC_E_NOMEM, cudaGetErrorString(err));
+      h->src_cap[d] = kd;
+    }
+    if (kd) WBC_CUDA_TRY(cudaMemcpyAsync(h->d_src[d], shard[d].data(), kd * 4, cudaMemcpyHostToDevice, st));
+    if (n) {
+      WBC_CUDA_TRY(cudaMemsetAsync(h->d_node[d], 0, uint64_t{n} * 8, st));
+      WBC_CUDA_TRY(cudaMemsetAsync(h->d_depth[d], 0, uint64_t{n} * 4, st));
+    }
+    if (edge && m) WBC_CUDA_TRY(cudaMemsetAsync(h->d_edge[d], 0, uint64_t{m} * 8, st));
+    // (a pageable H2D copy is staged before cudaMemcpyAsync returns: the
+    // shard may go out of scope; the devices run concurrently)
+    const int rc = launch_run(g, h->d_src[d], kd, edge, h->d_node[d], edge ? h->d_edge[d] : nullptr,
+                              h->d_depth[d], st, false, false);
+    if (rc) return rc;
+  }
+  // ---- the one collective: sum node / edge BC, max depth over devices
+  if (h->use_nccl) {  // (a forced single-device comm runs it too)
+    const NcclApi& nc = nccl_api();
+    nc.GroupStart();
+    ncclResult_t r = ncclSuccess;
+    for (size_t d = 0; d < D && r == ncclSuccess; ++d) {
+      r = nc.AllReduce(h->d_node[d], h->d_node[d], n, ncclFloat64, ncclSum, h->comm[d], h->st[d]);
+      if (r == ncclSuccess && edge)
+        r = nc.AllReduce(h->d_edge[d], h->d_edge[d], m, ncclFloat64, ncclSum, h->comm[d], h->st[d]);
+      if (r == ncclSuccess)
+        r = nc.AllReduce(h->d_depth[d], h->d_depth[d], n, ncclUint32, ncclMax, h->comm[d], h->st[d]);
+    }
+    const ncclResult_t r2 = nc.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return set_error(WBC_E_CUDA, std::string("ncclAllReduce: ") + nc.GetErrorString(r != ncclSuccess ? r : r2));
+  } else if (D > 1) {
+    for (size_t d = 1; d < D; ++d) {  // partials complete before the peer copies
+      WBC_CUDA_TRY(cudaSetDevice(h->g[d]->device));
+      WBC_CUDA_TRY(cudaStreamSynchronize(h->st[d]));
+    }
+    const int d0 = h->g[0]->device;
+    WBC_CUDA_TRY(cudaSetDevice(d0));
+    for (size_t d = 1; d < D; ++d) {
+      const int dd = h->g[d]->device;
+      WBC_CUDA_TRY(cudaMemcpyPeerAsync(h->d_tmp, d0, h->d_node[d], dd, uint64_t{n} * 8, h->st[0]));
+      wbc_dev::add_f64_kernel<<<launch_grid(n), 256, 0, h->st[0]>>>(h->d_node[0], h->d_tmp, n);
+      WBC_CUDA_TRY(cudaMemcpyPeerAsync(h->d_tmp32, d0, h->d_depth[d], dd, uint64_t{n} * 4, h->st[0]));
+      wbc_dev::max_u32_kernel<<<launch_grid(n), 256, 0, h->st[0]>>>(h->d_depth[0], h->d_tmp32, n);
+      if (edge) {
+        WBC_CUDA_TRY(cudaMemcpyPeerAsync(h->d_tmp, d0, h->d_edge[d], dd, uint64_t{m} * 8, h->st[0]));
+        wbc_dev::add_f64_kernel<<<launch_grid(m), 256, 0, h->st[0]>>>(h->d_edge[0], h->d_tmp, m);
+      }
+      WBC_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  WBC_CUDA_TRY(cudaSetDevice(h->g[0]->device));
+  const cudaStream_t s0 = h->st[0];
+  int rc = WBC_OK;
+  if (flags & WBC_HALVED) {  // engine.cpp:451-454
+    if ((rc = scale_async(h->d_node[0], n, 0.5, s0))) return rc;
+    if (edge && (rc = scale_async(h->d_edge[0], m, 0.5, s0))) return rc;
+  }
+  if (n) {
+    WBC_CUDA_TRY(cudaMemcpyAsync(node_bc, h->d_node[0], uint64_t{n} * 8, cudaMemcpyDeviceToHost, s0));
+    if (depth_per_source)
+      WBC_CUDA_TRY(cudaMemcpyAsync(depth_per_source, h->d_depth[0], uint64_t{n} * 4, cudaMemcpyDeviceToHost, s0));
+  }
+  if (edge && m) WBC_CUDA_TRY(cudaMemcpyAsync(edge_bc, h->d_edge[0], uint64_t{m} * 8, cudaMemcpyDeviceToHost, s0));
+  WBC_CUDA_TRY(cudaStreamSynchronize(s0));
+  if (elapsed_s) *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return WBC_OK;
 }
 

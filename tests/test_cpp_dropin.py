@@ -27,3 +27,11 @@ def test_cpp_dropin_cpu(binary):
 def test_cpp_dropin_gpu(binary):
     r = subprocess.run([binary, "gpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_gpu_sharded(binary):
+    """The same C++ checks with bc_parallel sharding its sources over two
+    replicas (one physical GPU listed twice -> device-copy reduction)."""
+    r = subprocess.run([binary, "gpu"], capture_output=True, text=True, env=dict(os.environ, WBC_GPU_DEVICES="0,0"))
+    assert r.returncode == 0, r.stdout + r.stderr
