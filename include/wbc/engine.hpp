@@ -4,10 +4,13 @@
 // engine.hpp (Strategy :14-29, parse_strategy :36-38, SettleRule :40-44,
 // EngineOptions :108-120, bc_parallel :122-130).  bc_parallel here runs the
 // per-source Brandes pipeline on a B200 through the C ABI in wbc_gpu.h; the
-// CPU schedule knobs (strategy, workers, strict_merge) are validated exactly
-// like the reference (engine.cpp:110-114,373-374) but do not change the GPU
-// schedule -- results are schedule-independent by the reference's own
-// contract (engine.hpp:127-129).
+// CPU schedule knobs (strategy, workers) are validated exactly like the
+// reference (engine.cpp:110-114,373-374) but do not change the GPU schedule --
+// results are schedule-independent by the reference's own contract
+// (engine.hpp:127-129).  strict_merge = true commits sources in list order and
+// sums each delta in the reference's slot order with strategy.lane_width
+// lanes: node/edge BC are then bitwise the reference's bc_parallel output
+// (WBC_STRICT_MERGE).
 #pragma once
 
 #include <cstdint>

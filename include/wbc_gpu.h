@@ -35,6 +35,15 @@ extern "C" {
 /* Flags for wbc_gpu_bc / wbc_gpu_bc_device. */
 #define WBC_HALVED 1u   /* Normalization::Halved (result.hpp:9-12): scale by 0.5 */
 #define WBC_EDGE_BC 2u  /* EngineOptions::compute_edge_bc (engine.hpp:111) */
+/* EngineOptions::strict_merge (engine.hpp:112-115, engine.cpp:389-413): per-
+ * source contributions are committed in source-list order and each source's
+ * delta is summed in the reference's own slot order with the strategy's lane
+ * width, so node / edge BC are bitwise the reference's bc_parallel output
+ * for that lane width (any worker count).  Runs in batches on the team
+ * kernel; slower than the default.  On a multi-GPU handle it runs on the
+ * first device only. */
+#define WBC_STRICT_MERGE 4u
+#define WBC_LANE_WIDTH(w) (((uint32_t)(w) & 0xFFu) << 8) /* Strategy::lane_width; 0 means 1 */
 
 typedef struct wbc_gpu_graph wbc_gpu_graph;
 

@@ -340,6 +340,8 @@ def _run_bc(fn, h, n: int, m: int, opt: Optional[EngineOptions]) -> BcResult:
         src = None
     flags = (L.WBC_HALVED if opt.normalization == Normalization.Halved else 0) | \
             (L.WBC_EDGE_BC if opt.compute_edge_bc else 0)
+    if opt.strict_merge:  # source-ordered commit, the reference's summation order (engine.cpp:389-413)
+        flags |= L.WBC_STRICT_MERGE | (opt.strategy.lane_width & 0xFF) << 8
     el = C.c_double()
     rc = fn(h, _p(src), 0 if src is None else len(src), flags, _p(node),
             _p(edge) if opt.compute_edge_bc else None, _p(depth), C.byref(el))

@@ -22,6 +22,7 @@ WBC_E_NOT_BUILT = -5
 WBC_E_PARSE = -6
 WBC_HALVED = 1
 WBC_EDGE_BC = 2
+WBC_STRICT_MERGE = 4
 WBC_MULTI_NO_NCCL = 1
 WBC_MULTI_FORCE_NCCL = 2
 

@@ -138,6 +138,17 @@ struct RunParams {
   unsigned long long* prof;  // null or kProfCounters per-run work counters
   const unsigned long long* k_dev;  // if set, the source count is read here (device-side)
   uint32_t team_base;               // first workspace slot of this launch (fill launches)
+  // strict merge (bc_team.cuh): delta per source by the reference's row scan
+  // (engine.cpp:183-212) into stage_node[i], edge terms into stage_edge[i];
+  // strict_merge_kernel then adds them in source order
+  uint32_t strict_lanes;            // 0: off; else the strategy's lane width
+  uint32_t strict_group;            // threads per vertex row (power of two, >= lanes, <= 32)
+  const uint32_t* ref_slots32;      // rows in the caller's slot order (relabelled ids)
+  const uint2* ref_slots64;
+  const uint32_t* ref_edge_id;
+  double* stage_node;               // k x n_stride
+  double* stage_edge;               // k x m, or null
+  uint64_t src_base;                // sources == null: source index i is vertex src_base + i
 };
 
 // Work counters (accumulated per source when RunParams::prof is set).
@@ -685,6 +696,26 @@ __global__ void scatter_add_kernel(double* out, const double* in, const uint32_t
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     out[perm[i]] += in[i];
+}
+
+// Ordered commit of a strict batch (engine.cpp:389-413): acc[v] += stage[i][v]
+// for i = 0..B-1 in source-list order, skipping v == source i when
+// `sources_dev` is set.  One thread per entry: the sum order is fixed.
+__global__ void strict_merge_kernel(double* acc, const double* stage, uint64_t stride, uint64_t len, int B,
+                                    const uint32_t* sources, uint64_t src_base, const uint32_t* inv,
+                                    int skip_source) {
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < len;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    double a = acc[v];
+    for (int i = 0; i < B; ++i) {
+      if (skip_source) {
+        const uint32_t so = sources ? __ldg(sources + i) : static_cast<uint32_t>(src_base + i);
+        if (__ldg(inv + so) == v) continue;
+      }
+      a = __dadd_rn(a, __ldcg(stage + i * stride + v));
+    }
+    acc[v] = a;
+  }
 }
 
 // dst += src (partial BC of another device, multi-GPU reduction without NCCL)

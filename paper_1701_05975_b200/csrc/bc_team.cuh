@@ -77,6 +77,7 @@ struct TeamShared {
   double acc[CH];
   TeamRed ring[4];     // used through rank 0's copy
   uint32_t bcast;
+  unsigned long long src_idx;  // launch-relative index of the current source (strict merge)
 };
 
 // Warp-aggregated append to a (possibly remote) counter; returns the slot.
@@ -256,8 +257,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
     tsync();
     const unsigned long long idx = prev().src;
     if (idx >= k_total) break;
-    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(idx);
+    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(p.src_base + idx);
     const uint32_t s = __ldg(p.inv + s_orig);
+    if (tid == 0) sh.src_idx = idx;  // read back by the strict backward (keeps idx out of registers)
     if (timing) t_last = clock64();
 
     // ---- init_state (engine.cpp:118-142): d = inf except d[s] = 0, level 0 = {s}
@@ -656,7 +658,64 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
     }
 
     // ---------------- dependency accumulation, deepest level first
-    if (!dag_over) {
+    if (p.strict_lanes) {
+      // The reference's own loop (engine.cpp:183-212), bit for bit: every
+      // vertex w of level L sums c = sw / sigma[v] * (1 + delta[v]) over its
+      // row in the caller's slot order, as `lanes` interleaved partial sums
+      // (slot j of the row feeds part[j % lanes]) combined in lane order.  A
+      // group of G threads takes one row, G consecutive slots per step; the
+      // hits of a step are folded into their lane's partial in slot order by
+      // a warp-uniform walk over the ballot mask.  Edge terms go to the
+      // source's stage row (one writer per edge and source).
+      GraphView gr = g;
+      gr.slots32 = p.ref_slots32;
+      gr.slots64 = p.ref_slots64;
+      const uint32_t LW = p.strict_lanes, G = p.strict_group;
+      const uint32_t lane = tid & 31, gl = lane & (G - 1), gb = lane & ~(G - 1);
+      constexpr uint32_t kWarps = TT / 32;
+      const uint32_t wid = gtid >> 5, per_warp = 32 / G;
+      const unsigned long long si = sh.src_idx;
+      double* const eacc = p.stage_edge ? p.stage_edge + si * static_cast<uint64_t>(g.m) : nullptr;
+      double* const sdelta = p.stage_node + si * p.ws.n_stride;  // this source's delta row
+      for (int L = static_cast<int>(nlev) - 1; L >= 0; --L) {
+        const uint32_t vb = __ldcg(lev + L), ve = static_cast<uint32_t>(L) + 1 == nlev ? ord_len : __ldcg(lev + L + 1);
+        for (uint32_t q0 = vb + wid * per_warp; q0 < ve; q0 += kWarps * per_warp) {
+          const uint32_t q = q0 + lane / G;
+          const bool has = q < ve;
+          const uint32_t w = has ? __ldcg(order + q) : 0u;
+          const uint32_t dw = has ? __ldcg(ord_d + q) : 0u;
+          const uint32_t rb = has ? __ldg(g.offsets + w) : 0u, re = has ? __ldg(g.offsets + w + 1) : 0u;
+          const double sw = has ? __ldcg(sigma + w) : 0.0;
+          double part = 0.0;
+          for (uint32_t st = 0; __any_sync(0xffffffffu, rb + st < re); st += G) {
+            const uint32_t e = rb + st + gl;
+            double c = 0.0;
+            bool hit = false;
+            if (e < re) {
+              uint32_t x, wt;
+              load_slot<PACKED>(gr, e, x, wt);
+              const uint32_t dx = dist.load(x);
+              if (dx != kInfDist && dx == dw + wt) {
+                hit = true;
+                c = __dmul_rn(__ddiv_rn(sw, __ldcg(sigma + x)), __dadd_rn(1.0, __ldcg(sdelta + x)));
+                if (eacc) eacc[__ldg(p.ref_edge_id + e)] = c;
+              }
+            }
+            uint32_t mask = __ballot_sync(0xffffffffu, hit);
+            while (mask) {
+              const uint32_t t = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const double ct = __shfl_sync(0xffffffffu, c, t);
+              if (lane == (t & ~(G - 1)) + (t & (G - 1)) % LW) part = __dadd_rn(part, ct);
+            }
+          }
+          double dsw = 0.0;
+          for (uint32_t j = 0; j < LW; ++j) dsw = __dadd_rn(dsw, __shfl_sync(0xffffffffu, part, gb + j));
+          if (has && gl == 0) sdelta[w] = dsw;
+        }
+        tsync();
+      }
+    } else if (!dag_over) {
       for (uint32_t L = nlev - 1; L >= 1; --L) {
         // dag_ends[nlev] is written by the leader in this very phase: use the register
         const uint32_t b = __ldcg(dag_ends + L), e = L + 1 == nlev ? dag_len : __ldcg(dag_ends + L + 1);

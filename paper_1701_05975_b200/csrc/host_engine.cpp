@@ -139,6 +139,7 @@ BcResult GpuBcEngine::bc(const EngineOptions& opt) const {
   uint32_t flags = 0;
   if (opt.normalization == Normalization::Halved) flags |= WBC_HALVED;
   if (opt.compute_edge_bc) flags |= WBC_EDGE_BC;
+  if (opt.strict_merge) flags |= WBC_STRICT_MERGE | WBC_LANE_WIDTH(opt.strategy.lane_width);
   const NodeId* src = nullptr;
   std::uint64_t k = 0;
   if (opt.sources) {

@@ -111,6 +111,13 @@ struct wbc_gpu_graph {
   uint2* d_slots64 = nullptr;
   uint32_t* d_minw = nullptr;
   uint32_t* d_edge_id = nullptr;
+  // the same rows in the caller's slot order (strict merge: the reference's
+  // summation order, engine.cpp:193-206)
+  uint32_t* d_ref_slots32 = nullptr;
+  uint2* d_ref_slots64 = nullptr;
+  uint32_t* d_ref_edge_id = nullptr;
+  double* d_stage = nullptr;  // strict batches: per-source delta rows, then edge rows
+  uint64_t stage_bytes = 0;
   uint32_t* d_perm = nullptr;  // device id -> caller id
   uint32_t* d_inv = nullptr;   // caller id -> device id
   std::vector<uint32_t> perm;  // host copy
@@ -131,6 +138,7 @@ struct wbc_gpu_graph {
   uint64_t tune_gen = 1, shape_gen = 0, ws_gen = 0;
   LaunchShape shape_cache{};
   int ws_want = -1, ws_slots_cached = 0;
+  int ws_shape_key = -1;      // launch shape the workspace was carved for
   int tune_fill = 0;          // opt-in: measured slower (R-MAT-24 C=16: 31.3 vs 32.5 GTEPS)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -171,7 +179,8 @@ struct wbc_gpu_graph {
                     (void*)d_edge_id, (void*)d_perm, (void*)d_inv, d_ws, (void*)d_counter,
                     (void*)d_abort_list, (void*)d_abort_count, (void*)d_counter2,
                     (void*)d_overflow, (void*)d_prof, (void*)d_node_dev, (void*)d_node,
-                    (void*)d_edge, (void*)d_depth, (void*)d_sources})
+                    (void*)d_edge, (void*)d_depth, (void*)d_sources, (void*)d_ref_slots32,
+                    (void*)d_ref_slots64, (void*)d_ref_edge_id, (void*)d_stage})
       cudaFree(p);
   }
 };
@@ -398,7 +407,8 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   // same knobs, same request, layout still carved: nothing to query or carve
-  if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want) {
+  const int shape_key = shape.cluster * 4096 + shape.threads * 2 + (shape.warp ? 1 : 0);
+  if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want && g->ws_shape_key == shape_key) {
     *slots_out = g->ws_slots_cached;
     return WBC_OK;
   }
@@ -514,6 +524,20 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   g->ws_gen = g->tune_gen;
   g->ws_want = want;
   g->ws_slots_cached = slots;
+  g->ws_shape_key = shape_key;
+  return WBC_OK;
+}
+
+// Lane width of a strict-merge request (0: not strict); validates it like
+// validate_strategy (engine.cpp:110-114).
+int strict_lanes_of(uint32_t flags, uint32_t* lanes) {
+  *lanes = 0;
+  if (!(flags & WBC_STRICT_MERGE)) return WBC_OK;
+  uint32_t w = (flags >> 8) & 0xFFu;
+  if (w == 0) w = 1;
+  if (w != 1 && w != 4 && w != 8 && w != 16 && w != 32)
+    return set_error(WBC_E_INVALID, "invalid lane width " + std::to_string(w) + " (expected 1, 4, 8, 16 or 32)");
+  *lanes = w;
   return WBC_OK;
 }
 
@@ -521,12 +545,22 @@ int launch_grid(uint64_t len) { return static_cast<int>(std::min<uint64_t>((len 
 
 // Enqueue one run: d_sources may be null (all vertices).  Accumulates node BC
 // (caller ids) into d_node, edge BC into d_edge; writes depth of run sources.
+int launch_strict(wbc_gpu_graph* g, const LaunchShape& shape, int slots, wbc_dev::RunParams p, uint64_t k,
+                  bool edge_bc, double* d_edge, uint32_t lanes, cudaStream_t stream);
+
 int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edge_bc,
                double* d_node, double* d_edge, uint32_t* d_depth, cudaStream_t stream,
-               bool single_slot, bool keep_state) {
+               bool single_slot, bool keep_state, uint32_t strict_lanes = 0) {
   g->stats[3] = 0;
   if (k == 0 || g->n == 0) return WBC_OK;
-  const LaunchShape shape = pick_shape(g);
+  LaunchShape shape = pick_shape(g);
+  if (strict_lanes && (shape.cluster == 0 || shape.warp)) {
+    // strict merge runs on the team kernel (its row-scan backward)
+    shape = LaunchShape{};
+    shape.cluster = 1;
+    shape.threads = g->skewed ? 1024 : 32;
+    shape.dyn_smem = wbc_dev::team_dyn_smem(shape.threads);
+  }
   const int want = single_slot ? 1 : static_cast<int>(std::min<uint64_t>(k, 1u << 30));
   int slots = 0;
   int rc = ensure_workspace(g, want, shape, &slots);
@@ -566,7 +600,10 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_node_dev, 0, uint64_t{g->n} * 8, stream));
   if (g->profiling)
     WBC_CUDA_TRY(cudaMemsetAsync(g->d_prof, 0, sizeof(unsigned long long) * wbc_dev::kProfCounters, stream));
-  if (shape.warp) {
+  if (strict_lanes) {
+    rc = launch_strict(g, shape, slots, p, k, edge_bc, d_edge, strict_lanes, stream);
+    if (rc) return rc;
+  } else if (shape.warp) {
     if (g->abort_cap < k) {
       cudaFree(g->d_abort_list);
       cudaError_t e2 = cudaSuccess;
@@ -660,7 +697,77 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  g->stats[3] = shape.warp ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
+  if (!strict_lanes) g->stats[3] = shape.warp ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
+  return WBC_OK;
+}
+
+// Strict merge (EngineOptions::strict_merge, engine.cpp:389-413): sources run
+// in batches of at most `slots`; each source's delta row (and edge terms) land
+// in a stage row, and strict_merge_kernel commits the batch in source order.
+// The result is bitwise the reference's for the same lane width.
+int launch_strict(wbc_gpu_graph* g, const LaunchShape& shape, int slots, wbc_dev::RunParams p, uint64_t k,
+                  bool edge_bc, double* d_edge, uint32_t lanes, cudaStream_t stream) {
+  const uint64_t ns = g->ws.n_stride, m = g->m;
+  const uint64_t per = ns * 8 + (edge_bc ? m * 8 : 0);
+  // several sources per team and batch: a batch ends with its slowest source
+  uint64_t B = std::min<uint64_t>(static_cast<uint64_t>(slots) * 8, k);
+  size_t free_b = 0, total_b = 0;
+  WBC_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t avail = free_b + g->stage_bytes;
+  const uint64_t reserve = (2ULL << 30) + total_b / 20;
+  B = std::max<uint64_t>(1, std::min<uint64_t>(B, avail > reserve ? (avail - reserve) / per : 1));
+  if (g->stage_bytes < B * per) {
+    cudaFree(g->d_stage);
+    g->d_stage = nullptr;
+    g->stage_bytes = 0;
+    cudaError_t err = cudaSuccess;
+    g->d_stage = dev_alloc<double>(B * per / 8, err);
+    if (err != cudaSuccess) return set_error(WBC_E_NOMEM, std::string("strict stage: ") + cudaGetErrorString(err));
+    g->stage_bytes = B * per;
+  }
+  // lanes per row: the next power of two of the mean degree, at least the lane width
+  const double avg = g->n ? 2.0 * m / g->n : 1.0;
+  uint32_t G = 1;
+  while (G < 32 && G < avg) G <<= 1;
+  p.strict_lanes = lanes;
+  p.strict_group = std::max(G, lanes);
+  p.ref_slots32 = g->d_ref_slots32;
+  p.ref_slots64 = g->d_ref_slots64;
+  p.ref_edge_id = g->d_ref_edge_id;
+  p.stage_node = g->d_stage;
+  p.stage_edge = edge_bc ? g->d_stage + B * ns : nullptr;
+  const uint32_t* d_sources = p.sources;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = shape.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<uint64_t>(B, slots)) * shape.cluster, 1, 1);
+  cfg.blockDim = dim3(shape.threads, 1, 1);
+  cfg.dynamicSmemBytes = shape.dyn_smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = shape.cluster > 1 ? 1 : 0;
+  uint64_t launches = 0;
+  for (uint64_t b0 = 0; b0 < k; b0 += B) {
+    const uint64_t kb = std::min<uint64_t>(B, k - b0);
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_stage, 0, kb * ns * 8, stream));
+    if (edge_bc) WBC_CUDA_TRY(cudaMemsetAsync(p.stage_edge, 0, kb * m * 8, stream));
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter, 0, sizeof(unsigned long long), stream));
+    p.sources = d_sources ? d_sources + b0 : nullptr;
+    p.src_base = d_sources ? 0 : b0;
+    p.k = kb;
+    WBC_CUDA_TRY(cudaLaunchKernelEx(&cfg, pick_team(shape.cluster, shape.threads, g->packed, g->profiling), p));
+    wbc_dev::strict_merge_kernel<<<launch_grid(g->n), 256, 0, stream>>>(
+        g->d_node_dev, g->d_stage, ns, g->n, static_cast<int>(kb), p.sources, p.src_base, g->d_inv, 1);
+    if (edge_bc && m)
+      wbc_dev::strict_merge_kernel<<<launch_grid(m), 256, 0, stream>>>(d_edge, p.stage_edge, m, m, static_cast<int>(kb),
+                                                                       nullptr, 0, nullptr, 0);
+    WBC_CUDA_TRY(cudaGetLastError());
+    launches += edge_bc && m ? 3 : 2;
+  }
+  g->stats[3] = launches + 1;  // + the scatter
   return WBC_OK;
 }
 
@@ -713,8 +820,8 @@ struct HostCsr {
   uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1;
   bool packed = true, skewed = false, has_edge_id = false;
   double hot_coverage_25k = 0;
-  std::vector<uint32_t> perm, inv, noff, slot32, eid, minw;
-  std::vector<uint2> slot64;
+  std::vector<uint32_t> perm, inv, noff, slot32, eid, minw, ref_slot32, ref_eid;
+  std::vector<uint2> slot64, ref_slot64;
 };
 
 int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
@@ -774,6 +881,9 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
   h.slot32.assign(h.packed ? slots : 0, 0);
   h.slot64.assign(h.packed ? 0 : slots, make_uint2(0, 0));
   h.eid.assign(edge_id ? slots : 0, 0);
+  h.ref_slot32.assign(h.packed ? slots : 0, 0);
+  h.ref_slot64.assign(h.packed ? 0 : slots, make_uint2(0, 0));
+  h.ref_eid.assign(edge_id ? slots : 0, 0);
   h.minw.assign(n, 0);
   double sum_minw = 0;
   uint64_t cnt_minw = 0;
@@ -796,8 +906,18 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
       const uint32_t v = perm[i];
       row.clear();
       for (uint32_t s = offsets[v]; s < offsets[v + 1]; ++s) row.emplace_back(inv[adjacency[s]], s);
-      std::sort(row.begin(), row.end());
       uint32_t o = noff[i];
+      for (const auto& [u, s] : row) {  // caller's order (strict merge)
+        const uint32_t w = static_cast<uint32_t>(weights[s]);
+        if (packed)
+          h.ref_slot32[o] = (u << wbits) | w;
+        else
+          h.ref_slot64[o] = make_uint2(u, w);
+        if (edge_id) h.ref_eid[o] = edge_id[s];
+        ++o;
+      }
+      std::sort(row.begin(), row.end());
+      o = noff[i];
       for (const auto& [u, s] : row) {
         const uint32_t w = static_cast<uint32_t>(weights[s]);
         if (packed)
@@ -865,7 +985,14 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
     else
       g->d_slots64 = dev_alloc<uint2>(slots, err);
   }
+  if (err == cudaSuccess) {
+    if (packed)
+      g->d_ref_slots32 = dev_alloc<uint32_t>(slots, err);
+    else
+      g->d_ref_slots64 = dev_alloc<uint2>(slots, err);
+  }
   if (err == cudaSuccess && h.has_edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
+  if (err == cudaSuccess && h.has_edge_id) g->d_ref_edge_id = dev_alloc<uint32_t>(slots, err);
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_NOMEM, std::string("graph upload: ") + cudaGetErrorString(err));
@@ -881,15 +1008,23 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
       err = cudaMemcpy(g->d_slots32, h.slot32.data(), slots * 4, cudaMemcpyHostToDevice);
     else
       err = cudaMemcpy(g->d_slots64, h.slot64.data(), slots * 8, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) {
+      if (packed)
+        err = cudaMemcpy(g->d_ref_slots32, h.ref_slot32.data(), slots * 4, cudaMemcpyHostToDevice);
+      else
+        err = cudaMemcpy(g->d_ref_slots64, h.ref_slot64.data(), slots * 8, cudaMemcpyHostToDevice);
+    }
     if (err == cudaSuccess && h.has_edge_id)
       err = cudaMemcpy(g->d_edge_id, h.eid.data(), slots * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess && h.has_edge_id)
+      err = cudaMemcpy(g->d_ref_edge_id, h.ref_eid.data(), slots * 4, cudaMemcpyHostToDevice);
   }
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_CUDA, std::string("graph upload: ") + cudaGetErrorString(err));
   }
-  g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 12 + slots * (packed ? 4 : 8) +
-                   (h.has_edge_id ? slots * 4 : 0);
+  g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 12 + 2 * slots * (packed ? 4 : 8) +
+                   (h.has_edge_id ? 2 * slots * 4 : 0);
   *out = g;
   return WBC_OK;
 }
@@ -993,11 +1128,13 @@ int wbc_gpu_bc_device(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, u
   if (edge && !g->d_edge_id)
     return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
   if (edge && !d_edge_bc && g->m) return set_error(WBC_E_INVALID, "edge_bc is required");
+  uint32_t lanes = 0;
+  int rc = strict_lanes_of(flags, &lanes);
+  if (rc) return rc;
   WBC_CUDA_TRY(cudaSetDevice(g->device));
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
   const uint64_t kk = d_sources ? k : g->n;
-  int rc = launch_run(g, d_sources, kk, edge, d_node_bc, d_edge_bc, d_depth_per_source, st, false,
-                      false);
+  rc = launch_run(g, d_sources, kk, edge, d_node_bc, d_edge_bc, d_depth_per_source, st, false, false, lanes);
   if (rc) return rc;
   if (flags & WBC_HALVED) {
     if ((rc = scale_async(d_node_bc, g->n, 0.5, st))) return rc;
@@ -1014,6 +1151,8 @@ int wbc_gpu_bc(wbc_gpu_graph* g, const uint32_t* sources, uint64_t k, uint32_t f
   if (edge && !edge_bc && g->m) return set_error(WBC_E_INVALID, "edge_bc is required");
   if (edge && !g->d_edge_id)
     return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
+  uint32_t lanes = 0;
+  if (const int rl = strict_lanes_of(flags, &lanes)) return rl;
   if (sources)  // resolve_sources (engine.cpp:349-361)
     for (uint64_t i = 0; i < k; ++i)
       if (sources[i] >= g->n)
@@ -1044,7 +1183,7 @@ int wbc_gpu_bc(wbc_gpu_graph* g, const uint32_t* sources, uint64_t k, uint32_t f
   }
   if (edge && g->m) WBC_CUDA_TRY(cudaMemsetAsync(g->d_edge, 0, uint64_t{g->m} * 8, st));
   int rc = launch_run(g, sources ? g->d_sources : nullptr, kk, edge, g->d_node, g->d_edge,
-                      g->d_depth, st, false, false);
+                      g->d_depth, st, false, false, lanes);
   if (rc) return rc;
   if (flags & WBC_HALVED) {  // engine.cpp:451-454
     if ((rc = scale_async(g->d_node, g->n, 0.5, st))) return rc;
@@ -1354,15 +1493,20 @@ int wbc_gpu_multi_bc(wbc_gpu_multi* h, const uint32_t* sources, uint64_t k, uint
   if (edge && !edge_bc && m) return set_error(WBC_E_INVALID, "edge_bc is required");
   if (edge && !h->d_edge[0])
     return set_error(WBC_E_INVALID, "edge BC requested but the graph was created without edge_id");
+  uint32_t lanes = 0;
+  if (const int rl = strict_lanes_of(flags, &lanes)) return rl;
   if (sources)  // resolve_sources (engine.cpp:349-361)
     for (uint64_t i = 0; i < k; ++i)
       if (sources[i] >= n) return set_error(WBC_E_INVALID, "bc_parallel: source id out of range");
   const auto t0 = std::chrono::steady_clock::now();
   const size_t D = h->g.size();
   const uint64_t total = sources ? k : n;
-  // strided shard of the source list per device (sources[i::D])
+  // strided shard of the source list per device (sources[i::D]); a strict
+  // merge keeps every source on the first device (one ordered commit), the
+  // others contribute exact zeros
   std::vector<std::vector<uint32_t>> shard(D);
-  for (uint64_t i = 0; i < total; ++i) shard[i % D].push_back(sources ? sources[i] : static_cast<uint32_t>(i));
+  for (uint64_t i = 0; i < total; ++i)
+    shard[lanes ? 0 : i % D].push_back(sources ? sources[i] : static_cast<uint32_t>(i));
   for (size_t d = 0; d < D; ++d) {
     wbc_gpu_graph* g = h->g[d];
     WBC_CUDA_TRY(cudaSetDevice(g->device));
@@ -1384,7 +1528,7 @@ int wbc_gpu_multi_bc(wbc_gpu_multi* h, const uint32_t* sources, uint64_t k, uint
     // (a pageable H2D copy is staged before cudaMemcpyAsync returns: the
     // shard may go out of scope; the devices run concurrently)
     const int rc = launch_run(g, h->d_src[d], kd, edge, h->d_node[d], edge ? h->d_edge[d] : nullptr,
-                              h->d_depth[d], st, false, false);
+                              h->d_depth[d], st, false, false, lanes);
     if (rc) return rc;
   }
   // ---- the one collective: sum node / edge BC, max depth over devices

@@ -13,6 +13,8 @@ ap.add_argument("--near", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--hot", type=int, default=-1)
 ap.add_argument("--prof", action="store_true")
+ap.add_argument("--strict", default="", help="strategy token: run with strict_merge (e.g. we, we-warp8)")
+ap.add_argument("--edge", action="store_true")
 ap.add_argument("--param", action="append", default=[], help="name=value")
 a = ap.parse_args()
 t = time.time()
@@ -34,7 +36,10 @@ for kv in a.param:
 print(gg.info(), flush=True)
 src = W.sample_sources(g.n, a.k, 1)
 for rep in range(a.reps):
-    r = gg.bc(W.EngineOptions(sources=src))
+    opt = W.EngineOptions(sources=src, compute_edge_bc=a.edge)
+    if a.strict:
+        opt.strict_merge, opt.strategy = True, W.parse_strategy(a.strict)
+    r = gg.bc(opt)
     st = gg.last_run_stats()
     print(f"rep {rep}: {r.elapsed*1e3:.1f} ms for {len(src)} sources -> {g.m*len(src)/r.elapsed/1e9:.2f} GTEPS; "
           f"{r.elapsed/len(src)*1e3:.3f} ms/src; stats {st}; depth mean {r.depth_per_source[src].mean():.1f}", flush=True)
