@@ -185,6 +185,8 @@ class RefLib:
         L.ref_csr_get.argtypes = [C.c_void_p] + [C.c_void_p] * 8
         L.ref_format_node_tsv.restype = C.c_uint64
         L.ref_format_node_tsv.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]
+        L.ref_format_edge_tsv.restype = C.c_uint64
+        L.ref_format_edge_tsv.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64]
 
     def _check(self, rc):
         if rc:
@@ -326,6 +328,13 @@ class RefLib:
                                               C.byref(elen), _ptr(acc)))
         return dict(dist=dist, sigma=sigma, delta=delta, depth=depth.value, order=order[: olen.value].copy(),
                     ends=ends[: elen.value].copy(), node_acc=acc)
+
+    def format_edge_tsv(self, g, edge_bc):
+        edge_bc = _f64(edge_bc)
+        L = self.lib.ref_format_edge_tsv(g.extra["handle"], _ptr(edge_bc), None, 0)
+        buf = C.create_string_buffer(int(L) + 1)
+        self.lib.ref_format_edge_tsv(g.extra["handle"], _ptr(edge_bc), buf, L)
+        return buf.raw[:L].decode()
 
     def format_node_tsv(self, g, node_bc):
         node_bc = _f64(node_bc)

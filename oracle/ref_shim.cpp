@@ -223,4 +223,13 @@ uint64_t ref_format_node_tsv(void* h, const double* node_bc, char* out, uint64_t
   return s.size();
 }
 
+uint64_t ref_format_edge_tsv(void* h, const double* edge_bc, char* out, uint64_t cap) {
+  const auto& g = *static_cast<wbc::CsrGraph*>(h);
+  wbc::BcResult r;
+  r.edge_bc.assign(edge_bc, edge_bc + g.m);
+  const std::string s = wbc::format_edge_bc_tsv(g, r);
+  if (cap >= s.size()) std::memcpy(out, s.data(), s.size());
+  return s.size();
+}
+
 }  // extern "C"

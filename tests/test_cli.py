@@ -145,3 +145,23 @@ def test_stats_depth(files):                                  # test_cli.cpp:170
     rc, out, _ = run(["stats", files["p3"], "--depth", "--seed", "1"])
     # depth_per_source of P3 is [3, 2, 3] (test_engine.cpp:376-380)
     assert rc == 0 and out == "n=3 m=2 max_degree=2 avg_degree=1.33333 avg_depth=2.66667\n"
+
+
+@pytest.mark.gpu
+def test_compute_strict_is_byte_identical_to_reference(files, ref):
+    """`--strict` (strict_merge): the TSV is byte-for-byte the reference's
+    bc_parallel + format_node_bc_tsv / format_edge_bc_tsv for the same lane width."""
+    u, v, w = ref.gen_er(250, 5.0, 9)
+    u, v, w = ref.assign_weights(u, v, w, 1, 12, 9)
+    path = str(files["d"] / "er250.txt")
+    with open(path, "w") as f:
+        f.write("".join(f"{a} {b} {c:.17g}\n" for a, b, c in zip(u.tolist(), v.tolist(), w.tolist())))
+    rc, out, _ = run(["compute", path, "--strict", "--strategy", "we-warp", "--lane-width", "8", "--edge-bc",
+                      "--sources-sample", "60", "--seed", "2"])
+    assert rc == 0
+    rg = ref.build_csr(u, v, w)
+    want = ref.bc_parallel(rg, "we-warp8", 4, sources=ref.sample_sources(rg.n, 60, 2), edge_bc=True,
+                           strict_merge=True)
+    exp = ref.format_node_tsv(rg, want["node_bc"]) + ref.format_edge_tsv(rg, want["edge_bc"])
+    ref.free_csr(rg)
+    assert out == exp
