@@ -44,6 +44,7 @@ extern "C" {
  * first device only. */
 #define WBC_STRICT_MERGE 4u
 #define WBC_LANE_WIDTH(w) (((uint32_t)(w) & 0xFFu) << 8) /* Strategy::lane_width; 0 means 1 */
+#define WBC_DETERMINISTIC WBC_STRICT_MERGE /* SURVEY.md §8(b) name for the same flag */
 
 typedef struct wbc_gpu_graph wbc_gpu_graph;
 

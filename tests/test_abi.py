@@ -80,3 +80,15 @@ def test_c_abi_error_paths_without_gpu():
     rc = lib.wbc_gpu_graph_create(2, 1, bad.ctypes.data, adj.ctypes.data, w.ctypes.data, mw.ctypes.data, None,
                                   -1, ctypes.byref(h))
     assert rc == _lib.WBC_E_INVALID
+
+
+def test_flag_and_status_constants_match_the_header():
+    """The Python mirror's flag / status values are the header's #defines."""
+    from paper_1701_05975_b200 import _lib
+    text = open(HEADER).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(WBC_[A-Z0-9_]+)\s+\(?(-?\d+)u?\)?", text)}
+    for name in ("WBC_OK", "WBC_E_INVALID", "WBC_E_UNSUPPORTED", "WBC_E_CUDA", "WBC_E_NOMEM", "WBC_HALVED",
+                 "WBC_EDGE_BC", "WBC_STRICT_MERGE", "WBC_MULTI_NO_NCCL", "WBC_MULTI_FORCE_NCCL"):
+        assert name in defs, name
+        assert getattr(_lib, name) == defs[name], name
+    assert "WBC_DETERMINISTIC WBC_STRICT_MERGE" in text
