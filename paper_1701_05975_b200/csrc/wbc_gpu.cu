@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "bc_flat.cuh"
 #include "bc_kernels.cuh"
 #include "bc_team.cuh"
 #include "bc_warp.cuh"
@@ -86,6 +87,7 @@ int set_error(int code, const std::string& msg) { return ::set_error(code, msg);
 struct LaunchShape {
   uint32_t near_width = 0; // 0: the graph's automatic width
   bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
+  bool flat = false;       // bc_flat_kernel (CTA per source, distance-first; team fallback)
   int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
   int threads = 128;
   uint32_t hot = 0;        // vertices with shared-memory distances
@@ -163,6 +165,10 @@ struct wbc_gpu_graph {
   int64_t tune_l2hot = -1;
   bool tune_near = false;      // near_width set explicitly (else the launch shape may adjust it)
   int tune_warp = 0;           // 1: bc_warp_kernel for flat graphs, 2: always (tests)
+  int tune_flat = -1;          // -1 auto (flat, large graphs), 0 off, 1 wherever eligible
+  uint32_t tune_flat_delta = 0;  // near-far window of bc_flat_kernel (0: max weight)
+  uint32_t max_degree = 0, max_minw = 0;
+  wbc_dev::FlatWs fw{};
   int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
   bool ws_team = false;        // workspace carries the team-kernel arrays
   bool profiling = false;
@@ -236,8 +242,35 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g);
 
 LaunchShape pick_shape(wbc_gpu_graph* g);
 
+// bc_flat_kernel: CTA size (two CTAs per SM: its phases are latency-bound)
+constexpr int kFlatT = 512;
+
+// bc_flat_kernel's bucket array: a power of two > max weight + max minw + 1.
+uint32_t flat_buckets(const wbc_gpu_graph* g) {
+  uint32_t b = 32;
+  while (b < static_cast<uint64_t>(g->max_weight) + g->max_minw + 2) b <<= 1;
+  return b;
+}
+
+bool flat_eligible(const wbc_gpu_graph* g) {
+  return g->n > 0 && g->max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg) &&
+         flat_buckets(g) <= static_cast<uint32_t>(wbc_dev::kFlatBuckets);
+}
+
 LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   LaunchShape s;
+  // Flat, large-diameter graphs (grid / road-like, degree <= 8, n >= 2^18)
+  // take the distance-first kernel: grid-2048 x 1024 sources 2.98 s vs 5.4 s
+  // for one-warp Eq. 4 teams, grid-512 2.93 vs 2.70 GTEPS; smaller graphs keep
+  // the teams, which fit every source in flight (grid-128: 2.08 vs 0.52).
+  const bool auto_flat = g->tune_flat < 0 && g->tune_cluster < 0 && g->tune_warp == 0 && g->tune_threads == 0 &&
+                         !g->skewed && g->n >= (1u << 18);
+  if ((g->tune_flat > 0 || auto_flat) && flat_eligible(g)) {
+    s.flat = true;
+    s.threads = kFlatT;
+    s.dyn_smem = flat_buckets(g) * 4;
+    return s;
+  }
   const uint64_t n = g->n;
   const bool tiny = n * 4 <= 24 * 1024;
   const bool warp_ok = true;  // distances >= 2^31-1 abort to the team kernel at run time
@@ -330,6 +363,37 @@ uint64_t ws_dcap(const wbc_gpu_graph* g, bool warp) {
   const uint64_t n = g->n;
   return warp ? round_up(n + n / 8 + 1024, 64) : round_up(n + n / 2 + 1024, 64);
 }
+uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
+  return ws_ns(g) * (4 + 8 + 8 + 4 + 4 + 4 + 16 + 4 + 4 + 8 * uint64_t{std::max<uint32_t>(1, g->max_degree)});
+}
+
+void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
+  const uint64_t ns = ws_ns(g);
+  auto carve = [&](uint64_t bytes) {
+    char* q = p;
+    p += bytes * slots;
+    return q;
+  };
+  wbc_dev::FlatWs& w = g->fw;
+  w.n_stride = ns;
+  w.sigma = reinterpret_cast<double*>(carve(ns * 8));
+  w.delta = reinterpret_cast<double*>(carve(ns * 8));
+  w.ivl_stride = std::max<uint32_t>(1, g->max_degree);
+  w.ivl = reinterpret_cast<uint2*>(carve(ns * 8 * w.ivl_stride));
+  w.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.npred = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.nsucc = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.flag = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.q0 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.q1 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.q3 = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.hist = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.sorted_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.delta_w = g->tune_flat_delta ? g->tune_flat_delta : std::max<uint32_t>(1, g->max_weight);
+  w.buckets = flat_buckets(g);
+}
+
 uint64_t ws_per_slot(const wbc_gpu_graph* g, bool warp, bool team, bool one_warp = false) {
   const uint64_t ns = ws_ns(g);
   if (warp) return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4) + ws_dcap(g, true) * 12;
@@ -407,7 +471,7 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   // same knobs, same request, layout still carved: nothing to query or carve
-  const int shape_key = shape.cluster * 4096 + shape.threads * 2 + (shape.warp ? 1 : 0);
+  const int shape_key = shape.cluster * 8192 + shape.threads * 4 + (shape.warp ? 1 : 0) + (shape.flat ? 2 : 0);
   if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want && g->ws_shape_key == shape_key) {
     *slots_out = g->ws_slots_cached;
     return WBC_OK;
@@ -415,9 +479,23 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   g->ws_gen = 0;
   const bool team = shape.cluster > 0;
   const bool one_warp = team && shape.cluster == 1 && shape.threads <= 32;
-  const uint64_t per_slot = ws_per_slot(g, shape.warp, team, one_warp);
+  const uint64_t per_slot = shape.flat ? ws_flat_per_slot(g) : ws_per_slot(g, shape.warp, team, one_warp);
   int slots = 0;
-  if (shape.warp) {
+  if (shape.flat) {
+    const void* f = reinterpret_cast<const void*>(g->packed ? wbc_dev::bc_flat_kernel<kFlatT, true>
+                                                             : wbc_dev::bc_flat_kernel<kFlatT, false>);
+    WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shape.dyn_smem)));
+    int per_sm = 0;
+    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kFlatT, shape.dyn_smem));
+    if (per_sm < 1) return set_error(WBC_E_CUDA, "flat kernel does not fit on an SM");
+    slots = per_sm * g->sm_count;
+    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(1, 32, g->packed)),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(wbc_dev::team_dyn_smem(32))));
+    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(1, 32, g->packed, true)),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(wbc_dev::team_dyn_smem(32))));
+  } else if (shape.warp) {
     for (const bool prof : {false, true}) {
       const void* f = reinterpret_cast<const void*>(
           g->packed ? (prof ? wbc_dev::bc_warp_kernel<true, true> : wbc_dev::bc_warp_kernel<true, false>)
@@ -464,7 +542,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
       if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
       slots = clusters;
     }
-  } else if (!shape.warp) {
+  } else if (!shape.warp && !shape.flat) {
     const KernelFn fn = pick_kernel(shape.threads, g->packed);
     for (const bool prof : {false, true})
       WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
@@ -504,7 +582,19 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   *slots_out = slots;
   char* base = static_cast<char*>(g->d_ws);
   g->last_warp = shape.warp;
-  if (shape.warp) {
+  if (shape.flat) {
+    // sources the flat kernel hands back run on one-warp teams over the same allocation
+    const uint64_t fb_per = ws_per_slot(g, false, true, true);
+    if (g->ws_bytes < fb_per) {
+      rc = ensure_bytes(g, fb_per);
+      if (rc) return rc;
+    }
+    carve_flat(g, static_cast<char*>(g->d_ws), slots);
+    g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
+    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
+    g->ws_slots = slots;
+    g->ws_team = false;
+  } else if (shape.warp) {
     // aborted sources re-run on one-warp teams over the same allocation
     const uint64_t fb_per = ws_per_slot(g, false, true, true);
     if (g->ws_bytes < fb_per) {
@@ -554,6 +644,13 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   g->stats[3] = 0;
   if (k == 0 || g->n == 0) return WBC_OK;
   LaunchShape shape = pick_shape(g);
+  if (shape.flat && (single_slot || strict_lanes)) {
+    // dumps and strict merges run on one-warp teams (their layouts / row-scan backward)
+    shape = LaunchShape{};
+    shape.cluster = 1;
+    shape.threads = 32;
+    shape.dyn_smem = wbc_dev::team_dyn_smem(32);
+  }
   if (strict_lanes && (shape.cluster == 0 || shape.warp)) {
     // strict merge runs on the team kernel (its row-scan backward)
     shape = LaunchShape{};
@@ -603,6 +700,41 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   if (strict_lanes) {
     rc = launch_strict(g, shape, slots, p, k, edge_bc, d_edge, strict_lanes, stream);
     if (rc) return rc;
+  } else if (shape.flat) {
+    if (g->abort_cap < k) {
+      cudaFree(g->d_abort_list);
+      cudaError_t e2 = cudaSuccess;
+      g->d_abort_list = dev_alloc<uint32_t>(k, e2);
+      if (e2 != cudaSuccess) {
+        g->abort_cap = 0;
+        return set_error(WBC_E_NOMEM, "abort list allocation failed");
+      }
+      g->abort_cap = k;
+    }
+    if (!g->d_abort_count) {
+      cudaError_t e2 = cudaSuccess;
+      g->d_abort_count = dev_alloc<unsigned long long>(2, e2);
+      if (e2 == cudaSuccess) g->d_counter2 = dev_alloc<unsigned long long>(1, e2);
+      if (e2 != cudaSuccess) return set_error(WBC_E_NOMEM, "counter allocation failed");
+    }
+    wbc_dev::FlatWs fw = g->fw;
+    fw.abort_list = g->d_abort_list;
+    fw.abort_count = g->d_abort_count;
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_abort_count, 0, sizeof(unsigned long long), stream));
+    WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter2, 0, sizeof(unsigned long long), stream));
+    const auto fk = g->packed ? wbc_dev::bc_flat_kernel<kFlatT, true> : wbc_dev::bc_flat_kernel<kFlatT, false>;
+    fk<<<slots, kFlatT, shape.dyn_smem, stream>>>(p, fw);
+    WBC_CUDA_TRY(cudaGetLastError());
+    // sources whose distances left the counting-sort range: one-warp teams
+    p.ws = g->ws_fb;
+    p.sources = g->d_abort_list;
+    p.src_base = 0;
+    p.k = k;
+    p.k_dev = g->d_abort_count;
+    p.counter = g->d_counter2;
+    p.hot = 0;
+    pick_team(1, 32, g->packed, g->profiling)<<<g->fb_slots, 32, wbc_dev::team_dyn_smem(32), stream>>>(p);
+    WBC_CUDA_TRY(cudaGetLastError());
   } else if (shape.warp) {
     if (g->abort_cap < k) {
       cudaFree(g->d_abort_list);
@@ -693,11 +825,12 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
   g->stats[1] = shape.threads * std::max(1, shape.cluster);
-  g->last_kernel = shape.warp ? std::string("bc_warp_kernel")
+  g->last_kernel = shape.flat ? std::string("bc_flat_kernel")
+                  : shape.warp ? std::string("bc_warp_kernel")
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  if (!strict_lanes) g->stats[3] = shape.warp ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
+  if (!strict_lanes) g->stats[3] = (shape.warp || shape.flat) ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
   return WBC_OK;
 }
 
@@ -817,7 +950,7 @@ namespace {
 // Host side of a graph upload, computed once and shared by every device of
 // a multi-GPU handle: validation, degree-descending relabel, packed slots.
 struct HostCsr {
-  uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1;
+  uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1, max_degree = 0, max_minw = 0;
   bool packed = true, skewed = false, has_edge_id = false;
   double hot_coverage_25k = 0;
   std::vector<uint32_t> perm, inv, noff, slot32, eid, minw, ref_slot32, ref_eid;
@@ -932,6 +1065,10 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
   // Near-window width: about a third of the mean minimum incident weight balances
   // near rescans against far refills.
   h.near_width = cnt_minw ? std::max<uint32_t>(1, static_cast<uint32_t>(sum_minw / cnt_minw / 3.0 + 0.5)) : 1;
+  for (uint32_t i = 0; i < n; ++i) {
+    h.max_degree = std::max(h.max_degree, h.noff[i + 1] - h.noff[i]);
+    if (h.minw[i] != wbc_dev::kInfDist) h.max_minw = std::max(h.max_minw, h.minw[i]);
+  }
   return WBC_OK;
 }
 
@@ -970,6 +1107,8 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   g->hot_coverage_25k = h.hot_coverage_25k;
   g->skewed = h.skewed;
   g->near_width = h.near_width;
+  g->max_degree = h.max_degree;
+  g->max_minw = h.max_minw;
   const bool packed = h.packed;
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
   if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);
@@ -1091,6 +1230,8 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
   else if (k == "warp") g->tune_warp = static_cast<int>(value);
   else if (k == "fill") g->tune_fill = static_cast<int>(value);
+  else if (k == "flat") g->tune_flat = static_cast<int>(value);
+  else if (k == "flat_delta") g->tune_flat_delta = static_cast<uint32_t>(std::max<int64_t>(0, value));
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }

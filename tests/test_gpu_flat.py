@@ -1,0 +1,96 @@
+"""GPU parity of the distance-first kernel for flat graphs (bc_flat.cuh,
+set_param("flat", 1)): near-far SSSP, dataflow sigma / delta, and the Eq. 4
+depth recovered from the distances by the threshold sweep.  Same bars as
+test_gpu_parity.py: BC 1e-9 relative, depth_per_source exact."""
+import numpy as np
+import pytest
+
+import fixtures as F
+from test_gpu_parity import check_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def flat_graph(W, g, delta=0):
+    gg = W.GpuGraph(g)
+    gg.set_param("flat", 1)
+    if delta:
+        gg.set_param("flat_delta", delta)
+    return gg
+
+
+def _cases(W):
+    yield "tie_square", F.tie_square_graph()
+    yield "path", F.path_graph(9)
+    yield "cycle", F.cycle_graph(7)
+    yield "star", F.star_graph(8)
+    yield "islands", F.graph_of([(0, 1, 1), (1, 2, 1), (10, 11, 1), (11, 12, 1)])
+    yield "grid_ties", W.build_csr(W.assign_weights(W.gen_grid(17, 23), 1, 3, 5))
+    yield "grid_unit", W.build_csr(W.assign_weights(W.gen_grid(20, 20), 1, 1, 5))
+    yield "grid_wide", W.build_csr(W.assign_weights(W.gen_grid(40, 31), 1, 1000, 7))
+    yield "tree", W.build_csr(F.random_tree(300, 9, 4))
+
+
+@pytest.mark.parametrize("delta", [0, 1, 37])
+def test_flat_matches_oracle(W, oracle, delta):
+    for name, g in _cases(W):
+        gg = flat_graph(W, g, delta)
+        try:
+            src = None if g.n <= 64 else W.sample_sources(g.n, 48, 3)
+            check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
+            assert gg.last_kernel() == "bc_flat_kernel", name
+        finally:
+            gg.close()
+
+
+def test_flat_halved_duplicates_and_all_sources(W, oracle):
+    g = W.build_csr(W.assign_weights(W.gen_grid(12, 15), 1, 50, 2))
+    gg = flat_graph(W, g)
+    try:
+        check_graph(W, oracle, g, edge=True, gg=gg)
+        src = np.array([5, 5, 0, 179, 5])
+        check_graph(W, oracle, g, sources=src, edge=True, halved=True, gg=gg)
+    finally:
+        gg.close()
+
+
+def test_flat_hands_long_distances_to_the_team_kernel(W, oracle):
+    """Distances beyond the counting-sort range (n_stride) abort to one-warp
+    teams before anything is accumulated."""
+    g = F.path_graph(40, w=1000.0)
+    gg = flat_graph(W, g)
+    try:
+        check_graph(W, oracle, g, edge=True, gg=gg)
+        assert gg.last_kernel() == "bc_flat_kernel"
+    finally:
+        gg.close()
+
+
+def test_flat_falls_back_when_ineligible(W, oracle):
+    """Degree above the sweep's 8 slots per vertex: the normal shapes run."""
+    g = F.star_graph(30)
+    gg = flat_graph(W, g)
+    try:
+        check_graph(W, oracle, g, edge=True, gg=gg)
+        assert gg.last_kernel() != "bc_flat_kernel"
+    finally:
+        gg.close()
+
+
+def test_flat_grid_sampled_vs_reference(W, ref):
+    el = W.assign_weights(W.gen_grid(96, 96), 1, 1000, 1)
+    g = W.build_csr(el)
+    rg = ref.build_csr(el.u, el.v, el.w)
+    try:
+        src = W.sample_sources(g.n, 64, 1)
+        want = ref.bc_parallel(rg, "we", 8, sources=src)
+        gg = flat_graph(W, g)
+        try:
+            r = gg.bc(W.EngineOptions(sources=src))
+        finally:
+            gg.close()
+        rel = np.abs(r.node_bc - want["node_bc"]) / np.maximum(1e-12, np.abs(want["node_bc"]))
+        assert (rel <= 1e-9).all()
+        assert np.array_equal(r.depth_per_source, want["depth"])
+    finally:
+        ref.free_csr(rg)
