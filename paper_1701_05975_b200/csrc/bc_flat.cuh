@@ -21,7 +21,8 @@
 //   D. delta the same way in reverse, with the reference's term
 //      sigma[u] / sigma[v] * (1 + delta[v]) (engine.cpp:201) and node / edge BC;
 //   E. a counting sort of the distances, then one warp sweeps the thresholds
-//      with a shared-memory bucket array (key -> largest successor distance).
+//      with a shared-memory bucket array (key -> largest successor distance),
+//      concurrently with C and D on the other warps.
 // Sources whose distances exceed the counting-sort range are handed to the
 // team kernel (abort list), before anything is accumulated.
 #pragma once
@@ -197,7 +198,10 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 
     tick(kProfCyclesRelax);
     if (p.prof && tid == 0) atomicAdd(p.prof + kProfRounds, static_cast<unsigned long long>(iter));
-    // ---- B. DAG degrees, reached count, max distance
+    // ---- B. the DAG: per vertex a successor mask (slots u->v with
+    // d(v) = d(u) + w) and a predecessor mask (d(u) = d(v) + w) in `flag`
+    // (free after A), successor counts, predecessor counts, reached count,
+    // max distance
     if (tid == 0) {
       s_reached = 0;
       s_maxd = 0;
@@ -210,17 +214,21 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         if (du == kInfDist) continue;
         ++reached;
         maxd = max(maxd, du);
-        uint32_t b, e, cnt = 0;
+        uint32_t b, e, sm = 0, pm = 0;
         row_of(u, b, e);
         for (uint32_t x = b; x < e; ++x) {
           uint32_t v, wt;
           load_slot<PACKED>(g, x, v, wt);
-          if (__ldcg(dist + v) == du + wt) {
-            ++cnt;
+          const uint32_t dv = __ldcg(dist + v);
+          if (dv == du + wt) {
+            sm |= 1u << (x - b);
             atomicAdd(npred + v, 1u);
+          } else if (dv != kInfDist && dv + wt == du) {
+            pm |= 1u << (x - b);
           }
         }
-        nsucc[u] = cnt;
+        nsucc[u] = __popc(sm);
+        flag[u] = sm | pm << 16;
       }
       reached = __reduce_add_sync(0xffffffffu, reached);
       maxd = __reduce_max_sync(0xffffffffu, maxd);
@@ -239,85 +247,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       continue;
     }
 
-    // ---- C. sigma, forward dataflow over the DAG
-    uint32_t* const qf = w.q0 + off;
-    for (uint32_t i = tid; i < reached; i += T) qf[i] = kFlatEmpty;
-    __syncthreads();
-    if (tid == 0) {
-      sigma[s] = 1.0;
-      s_head = 0;
-      s_tail = 1;
-      st_vol(qf, s);
-    }
-    __syncthreads();
-    for (;;) {
-      const uint32_t i = atomicAdd(&s_head, 1u);
-      if (i >= reached) break;
-      uint32_t u;
-      while ((u = ld_vol(qf + i)) == kFlatEmpty) __nanosleep(32);
-      __threadfence_block();
-      const double su = __ldcg(sigma + u);
-      const uint32_t du = __ldcg(dist + u);
-      uint32_t b, e;
-      row_of(u, b, e);
-      for (uint32_t x = b; x < e; ++x) {
-        uint32_t v, wt;
-        load_slot<PACKED>(g, x, v, wt);
-        if (__ldcg(dist + v) != du + wt) continue;
-        atomicAdd(sigma + v, su);
-        __threadfence_block();
-        if (atomicSub(npred + v, 1u) == 1u) {
-          __threadfence_block();
-          st_vol(qf + atomicAdd(&s_tail, 1u), v);
-        }
-      }
-    }
-    __syncthreads();
-
-    tick(kProfCyclesSettle);
-    // ---- D. delta, reverse dataflow; node / edge BC
-    uint32_t* const qb = w.q1 + off;
-    for (uint32_t i = tid; i < reached; i += T) qb[i] = kFlatEmpty;
-    if (tid == 0) {
-      s_head = 0;
-      s_tail = 0;
-    }
-    __syncthreads();
-    for (uint32_t u = tid; u < n; u += T)  // the DAG's sinks start the sweep
-      if (__ldcg(dist + u) != kInfDist && nsucc[u] == 0) st_vol(qb + atomicAdd(&s_tail, 1u), u);
-    __syncthreads();
-    for (;;) {
-      const uint32_t i = atomicAdd(&s_head, 1u);
-      if (i >= reached) break;
-      uint32_t v;
-      while ((v = ld_vol(qb + i)) == kFlatEmpty) __nanosleep(32);
-      __threadfence_block();
-      const double dvv = __ldcg(delta + v);
-      const double sv = __ldcg(sigma + v);
-      const uint32_t dv = __ldcg(dist + v);
-      if (v != s) atomicAdd(p.node_bc + v, dvv);
-      uint32_t b, e;
-      row_of(v, b, e);
-      for (uint32_t x = b; x < e; ++x) {
-        uint32_t u, wt;
-        load_slot<PACKED>(g, x, u, wt);
-        const uint32_t du = __ldcg(dist + u);
-        if (du == kInfDist || du + wt != dv) continue;
-        // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
-        const double c = __ldcg(sigma + u) / sv * (1.0 + dvv);
-        atomicAdd(delta + u, c);
-        if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + x), c);
-        __threadfence_block();
-        if (atomicSub(nsucc + u, 1u) == 1u) {
-          __threadfence_block();
-          st_vol(qb + atomicAdd(&s_tail, 1u), u);
-        }
-      }
-    }
-    __syncthreads();
-
-    tick(kProfCyclesBackward);
-    // ---- E. depth: counting sort of distances, then the threshold sweep
+    // ---- E1. counting sort of the distances and the sweep input
     for (uint32_t i = tid; i <= maxd; i += T) hist[i] = 0;
     __syncthreads();
     for (uint32_t u = tid; u < n; u += T) {
@@ -401,8 +331,11 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     __syncthreads();
     for (uint32_t i = tid; i < w.buckets; i += T) bucket[i] = 0;
     __syncthreads();
-    tick(kProfNearScanned);  // counting sort + sweep input
+    tick(kProfNearScanned);
+    // Warp 0 sweeps the Eq. 4 thresholds (E2) while the other warps run the
+    // sigma (C) and delta (D) dataflows; they synchronise on named barrier 1.
     if (wid == 0) {
+      // ---- E2. threshold sweep
       const uint32_t B = w.buckets, M = B - 1;
       // bucket[k & M] = 1 + largest d(v) over inserted slots with key k; the
       // key is live at threshold tau iff that d(v) >= tau
@@ -487,6 +420,77 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         prefetch(pos);
       }
       if (lane == 0 && p.depth) p.depth[s_orig] = levels;
+    } else {
+      constexpr uint32_t TG = T - 32;  // dataflow threads
+      const uint32_t gt = tid - 32;
+      auto gsync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(TG) : "memory"); };
+      // ---- C. sigma, forward dataflow over the DAG
+      uint32_t* const qf = w.q0 + off;
+      for (uint32_t i = gt; i < reached; i += TG) qf[i] = kFlatEmpty;
+      gsync();
+      if (gt == 0) {
+        sigma[s] = 1.0;
+        s_head = 0;
+        s_tail = 1;
+        st_vol(qf, s);
+      }
+      gsync();
+      for (;;) {
+        const uint32_t i = atomicAdd(&s_head, 1u);
+        if (i >= reached) break;
+        uint32_t u;
+        while ((u = ld_vol(qf + i)) == kFlatEmpty) __nanosleep(32);
+        __threadfence_block();
+        const double su = __ldcg(sigma + u);
+        const uint32_t b = __ldg(g.offsets + u);
+        for (uint32_t sm = __ldcg(flag + u) & 0xFFFFu; sm; sm &= sm - 1) {
+          uint32_t v, wt;
+          load_slot<PACKED>(g, b + __ffs(sm) - 1, v, wt);
+          atomicAdd(sigma + v, su);
+          __threadfence_block();
+          if (atomicSub(npred + v, 1u) == 1u) {
+            __threadfence_block();
+            st_vol(qf + atomicAdd(&s_tail, 1u), v);
+          }
+        }
+      }
+      gsync();
+      // ---- D. delta, reverse dataflow; node / edge BC
+      uint32_t* const qb = w.q1 + off;
+      for (uint32_t i = gt; i < reached; i += TG) qb[i] = kFlatEmpty;
+      if (gt == 0) {
+        s_head = 0;
+        s_tail = 0;
+      }
+      gsync();
+      for (uint32_t u = gt; u < n; u += TG)  // the DAG's sinks start the sweep
+        if (__ldcg(dist + u) != kInfDist && nsucc[u] == 0) st_vol(qb + atomicAdd(&s_tail, 1u), u);
+      gsync();
+      for (;;) {
+        const uint32_t i = atomicAdd(&s_head, 1u);
+        if (i >= reached) break;
+        uint32_t v;
+        while ((v = ld_vol(qb + i)) == kFlatEmpty) __nanosleep(32);
+        __threadfence_block();
+        const double dvv = __ldcg(delta + v);
+        const double sv = __ldcg(sigma + v);
+        if (v != s) atomicAdd(p.node_bc + v, dvv);
+        const uint32_t b = __ldg(g.offsets + v);
+        for (uint32_t pm = __ldcg(flag + v) >> 16; pm; pm &= pm - 1) {
+          const uint32_t x = b + __ffs(pm) - 1;
+          uint32_t u, wt;
+          load_slot<PACKED>(g, x, u, wt);
+          // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
+          const double c = __ldcg(sigma + u) / sv * (1.0 + dvv);
+          atomicAdd(delta + u, c);
+          if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + x), c);
+          __threadfence_block();
+          if (atomicSub(nsucc + u, 1u) == 1u) {
+            __threadfence_block();
+            st_vol(qb + atomicAdd(&s_tail, 1u), u);
+          }
+        }
+      }
     }
     __syncthreads();
     tick(kProfRefills);
