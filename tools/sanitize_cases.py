@@ -22,13 +22,20 @@ cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("team C=4", kron, {"cluster": 4}),
          ("one-warp team", grid, {"cluster": 1, "threads": 32}),
          ("warp kernel + fallback", kron, {"warp": 2}),
-         ("warp kernel", grid, {"warp": 2})]
+         ("warp kernel", grid, {"warp": 2}),
+         ("flat kernel", grid, {"flat": 1}),
+         ("flat kernel + team fallback", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
+         ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8})]
 for name, g, params in cases:
     src = W.sample_sources(g.n, 6, 1)
     gg = W.GpuGraph(g, 0)
+    strict = params.pop("_strict", 0)
     for k, v in params.items():
         gg.set_param(k, v)
-    r = gg.bc(W.EngineOptions(sources=src, compute_edge_bc=True))
+    opt = W.EngineOptions(sources=src, compute_edge_bc=True)
+    if strict:
+        opt.strict_merge, opt.strategy = True, W.Strategy(W.FrontierMode.Queue, strict)
+    r = gg.bc(opt)
     kern = gg.last_kernel()
     gg.close()
     node, edge, depth = O.bc_eq4(g, sources=src, edge_bc=True)
