@@ -133,7 +133,13 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
 
 /* Named tuning parameter (experiments/benches): "threads", "slots",
  * "near_width", "hot" (shared-memory distance entries; -1 auto), "l2hot"
- * (ids whose distance accesses carry an L2 evict-last hint; -1 auto). */
+ * (ids whose distance accesses carry an L2 evict-last hint; -1 auto),
+ * "cluster" (team kernel CTAs per source; -1 auto, 0 per-CTA kernel),
+ * "warp" (1: one-warp kernel for flat graphs, 2: always), "fill" (2-CTA
+ * fill clusters beside C >= 4), "flat" (distance-first kernel for flat
+ * graphs: -1 auto = degree <= 8 and n >= 2^18, 0 off, 1 wherever eligible),
+ * "flat_delta" (its near-far window; 0 = max weight).  Unknown names return
+ * WBC_E_INVALID. */
 int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value);
 
 /* Work counters of subsequent runs (off by default; a few atomics per
