@@ -305,6 +305,8 @@ def main():
     ap.add_argument("--workload", default="rmat20", choices=sorted(WORKLOADS))
     ap.add_argument("--sources", type=int, default=0, help="override the workload's source count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-baseline-large", action="store_true",
+                    help="also time the reference on R-MAT-24 (its own generator + CSR build take ~10 min)")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--near", type=int, default=0)
@@ -452,7 +454,12 @@ def main():
                              d2h_bytes_per_step=int(d2h), api="wbc_gpu_bc (host buffers)"),
                     roofline=roofline, clocks=clk, gpu_launches=int(launches),
                     run_stats=gg.last_run_stats(), bc_checksum=bc_sum)
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and args.workload == "rmat24" and not args.cpu_baseline_large:
+            line["cpu_baseline"] = dict(value=None, unit="GTEPS", cores=os.cpu_count(), kind="reference",
+                                        sample="skipped: the reference's own scale-24 generator and CSR build "
+                                               "take ~10 min on the host (--cpu-baseline-large runs it); "
+                                               "the rmat20 line carries the CPU ratio")
+        elif not args.no_cpu_baseline and world == 1:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.workload, wl)
             except Exception as ex:  # reported, never fatal
