@@ -94,3 +94,29 @@ def test_flat_grid_sampled_vs_reference(W, ref):
         assert np.array_equal(r.depth_per_source, want["depth"])
     finally:
         ref.free_csr(rg)
+
+
+def test_flat_graph_strict_merge_and_dumps_use_teams(W, ref, oracle):
+    """A strict merge (bitwise reference order) and the single-source dumps run
+    on one-warp teams even where the flat kernel is selected."""
+    el = W.assign_weights(W.gen_grid(20, 26), 1, 9, 4)
+    g = W.build_csr(el)
+    rg = ref.build_csr(el.u, el.v, el.w)
+    gg = flat_graph(W, g)
+    try:
+        src = W.sample_sources(g.n, 40, 2)
+        want = ref.bc_parallel(rg, "we-warp4", 3, sources=src, edge_bc=True, strict_merge=True)
+        r = gg.bc(W.EngineOptions(strategy=W.parse_strategy("we-warp4"), compute_edge_bc=True, strict_merge=True,
+                                  sources=src))
+        assert np.array_equal(r.node_bc.view(np.uint64), want["node_bc"].view(np.uint64))
+        assert np.array_equal(r.edge_bc.view(np.uint64), want["edge_bc"].view(np.uint64))
+        d = gg.dump_source(7)
+        o = oracle.eq4_source(g, 7)
+        assert np.array_equal(d["dist"], o["dist"]) and np.array_equal(d["sigma"], o["sigma"])
+        assert d["depth"] == o["depth"]
+        r2 = gg.bc(W.EngineOptions(sources=src))
+        assert gg.last_kernel() == "bc_flat_kernel"
+        assert np.abs(r2.node_bc - r.node_bc).max() <= 1e-9 * max(1.0, np.abs(r.node_bc).max())
+    finally:
+        gg.close()
+        ref.free_csr(rg)
