@@ -168,6 +168,7 @@ struct wbc_gpu_graph {
   int tune_flat = -1;          // -1 auto (flat, large graphs), 0 off, 1 wherever eligible
   uint32_t tune_flat_delta = 0;  // near-far window of bc_flat_kernel (0: max weight)
   uint32_t max_degree = 0, max_minw = 0;
+  bool symmetric = false;
   wbc_dev::FlatWs fw{};
   int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
   bool ws_team = false;        // workspace carries the team-kernel arrays
@@ -253,7 +254,7 @@ uint32_t flat_buckets(const wbc_gpu_graph* g) {
 }
 
 bool flat_eligible(const wbc_gpu_graph* g) {
-  return g->n > 0 && g->max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg) &&
+  return g->n > 0 && g->symmetric && g->max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg) &&
          flat_buckets(g) <= static_cast<uint32_t>(wbc_dev::kFlatBuckets);
 }
 
@@ -951,6 +952,7 @@ namespace {
 // a multi-GPU handle: validation, degree-descending relabel, packed slots.
 struct HostCsr {
   uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1, max_degree = 0, max_minw = 0;
+  bool symmetric = false;  // every slot u->v (w) has a twin v->u (w); checked for low-degree graphs
   bool packed = true, skewed = false, has_edge_id = false;
   double hot_coverage_25k = 0;
   std::vector<uint32_t> perm, inv, noff, slot32, eid, minw, ref_slot32, ref_eid;
@@ -1069,6 +1071,28 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
     h.max_degree = std::max(h.max_degree, h.noff[i + 1] - h.noff[i]);
     if (h.minw[i] != wbc_dev::kInfDist) h.max_minw = std::max(h.max_minw, h.minw[i]);
   }
+  // The flat kernel's dataflows count DAG edges from both ends; a caller CSR
+  // whose rows are not mirror images (not from build_csr) must not reach it.
+  if (h.max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg)) {
+    h.symmetric = true;
+    for (uint32_t u = 0; u < n && h.symmetric; ++u)
+      for (uint32_t e = h.noff[u]; e < h.noff[u + 1] && h.symmetric; ++e) {
+        const uint32_t v = packed ? h.slot32[e] >> wbits : h.slot64[e].x;
+        const uint32_t w = packed ? h.slot32[e] & ((wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1)) : h.slot64[e].y;
+        uint32_t twins = 0, same = 0;
+        for (uint32_t f = h.noff[v]; f < h.noff[v + 1]; ++f) {
+          const uint32_t x = packed ? h.slot32[f] >> wbits : h.slot64[f].x;
+          const uint32_t y = packed ? h.slot32[f] & ((wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1)) : h.slot64[f].y;
+          twins += x == u && y == w;
+        }
+        for (uint32_t f = h.noff[u]; f < h.noff[u + 1]; ++f) {
+          const uint32_t x = packed ? h.slot32[f] >> wbits : h.slot64[f].x;
+          const uint32_t y = packed ? h.slot32[f] & ((wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1)) : h.slot64[f].y;
+          same += x == v && y == w;
+        }
+        h.symmetric = twins == same && u != v;
+      }
+  }
   return WBC_OK;
 }
 
@@ -1109,6 +1133,7 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   g->near_width = h.near_width;
   g->max_degree = h.max_degree;
   g->max_minw = h.max_minw;
+  g->symmetric = h.symmetric;
   const bool packed = h.packed;
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
   if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);

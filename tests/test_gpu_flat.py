@@ -120,3 +120,27 @@ def test_flat_graph_strict_merge_and_dumps_use_teams(W, ref, oracle):
     finally:
         gg.close()
         ref.free_csr(rg)
+
+
+def test_flat_refuses_asymmetric_rows(W):
+    """A caller CSR whose rows are not mirror images (not from build_csr) never
+    reaches the flat kernel: its dataflows count DAG edges from both ends."""
+    u32 = lambda *a: np.array(a, np.uint32)
+    f64 = lambda *a: np.array(a, np.float64)
+    # rows 0->1 (w1), 1->0 (w1), 1->2 (w2), 2->1 (w3: the twin disagrees)
+    g = W.CsrGraph(n=3, m=2, offsets=u32(0, 1, 3, 4), adjacency=u32(1, 0, 2, 1), weights=f64(1, 1, 2, 3),
+                   edge_id=u32(0, 0, 1, 1), min_incident_weight=f64(1, 1, 3), original_id=np.arange(3, dtype=np.uint64),
+                   edge_u=u32(0, 1), edge_v=u32(1, 2))
+    gg = flat_graph(W, g)
+    try:
+        gg.bc(W.EngineOptions())
+        assert gg.last_kernel() != "bc_flat_kernel"
+    finally:
+        gg.close()
+    ok = W.build_csr(W.assign_weights(W.gen_grid(5, 5), 1, 9, 1))
+    gg = flat_graph(W, ok)
+    try:
+        gg.bc(W.EngineOptions())
+        assert gg.last_kernel() == "bc_flat_kernel"
+    finally:
+        gg.close()
