@@ -137,21 +137,36 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       const uint32_t thr32 = thr >= kInfDist ? kInfDist : static_cast<uint32_t>(thr);
       if (near_len) {
         // relax every near vertex (thread per vertex: flat rows are short)
+        // (the row's slot words, then its distance gathers, then its atomics:
+        // each stage's loads are in flight together)
         for (uint32_t i = tid; i < near_len; i += T) {
           const uint32_t v = nq[i];
           const uint32_t dv = __ldcg(dist + v);
           uint32_t b, e;
           row_of(v, b, e);
-          for (uint32_t x = b; x < e; ++x) {
-            uint32_t u, wt;
-            load_slot<PACKED>(g, x, u, wt);
-            const uint32_t nd = dv + wt;
-            if (nd >= __ldcg(dist + u)) continue;
-            const uint32_t old = atomicMin(dist + u, nd);
-            if (nd >= old) continue;
-            if (nd < thr32) {
+          uint32_t us[kFlatMaxDeg], nd[kFlatMaxDeg], old[kFlatMaxDeg];
+#pragma unroll
+          for (int x = 0; x < kFlatMaxDeg; ++x) {
+            us[x] = kFlatEmpty;
+            nd[x] = kInfDist;
+            if (b + x < e) {
+              uint32_t wt;
+              load_slot<PACKED>(g, b + x, us[x], wt);
+              nd[x] = dv + wt;
+            }
+          }
+#pragma unroll
+          for (int x = 0; x < kFlatMaxDeg; ++x)
+            if (us[x] != kFlatEmpty && nd[x] >= __ldcg(dist + us[x])) us[x] = kFlatEmpty;
+#pragma unroll
+          for (int x = 0; x < kFlatMaxDeg; ++x) old[x] = us[x] != kFlatEmpty ? atomicMin(dist + us[x], nd[x]) : 0u;
+#pragma unroll
+          for (int x = 0; x < kFlatMaxDeg; ++x) {
+            if (us[x] == kFlatEmpty || nd[x] >= old[x]) continue;
+            const uint32_t u = us[x];
+            if (nd[x] < thr32) {
               if (atomicExch(flag + u, iter + 1) != iter + 1) nn[atomicAdd(&R[0], 1u)] = u;
-            } else if (old == kInfDist) {
+            } else if (old[x] == kInfDist) {
               fq[far_len + atomicAdd(&R[1], 1u)] = u;
             }
           }
