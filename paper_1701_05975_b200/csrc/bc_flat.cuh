@@ -62,7 +62,11 @@ __device__ __forceinline__ void st_vol(uint32_t* a, uint32_t v) { *reinterpret_c
 
 template <int T, bool PACKED>
 __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p, const FlatWs w) {
-  // p.prof: per-phase SM cycles (init, A, B, C, D -> kProfCyclesInit.., E -> kProfRefills)
+  // p.prof: per-phase SM cycles of thread 0, reusing the team kernel's counter
+  // slots: init -> kProfCyclesInit, A -> kProfCyclesRelax, B ->
+  // kProfCyclesThreshold, E1 histogram -> kProfFarScanned, scan ->
+  // kProfImprovements, scatter + sweep input -> kProfNearScanned, E2 || C/D ->
+  // kProfRefills; A's phases -> kProfRounds
   unsigned long long t_last = 0;
   auto tick = [&](int slot) {
     if (p.prof && threadIdx.x == 0) {
@@ -265,12 +269,18 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     // ---- E1. counting sort of the distances and the sweep input
     for (uint32_t i = tid; i <= maxd; i += T) hist[i] = 0;
     __syncthreads();
-    for (uint32_t u = tid; u < n; u += T) {
-      const uint32_t du = __ldcg(dist + u);
-      if (du != kInfDist) atomicAdd(hist + du, 1u);
+    constexpr int kH = 8;  // vertices per thread and step: their loads in flight together
+    for (uint32_t u0 = tid; u0 < n; u0 += T * kH) {
+      uint32_t du[kH];
+#pragma unroll
+      for (int j = 0; j < kH; ++j) du[j] = u0 + j * T < n ? __ldcg(dist + u0 + j * T) : kInfDist;
+#pragma unroll
+      for (int j = 0; j < kH; ++j)
+        if (du[j] != kInfDist) atomicAdd(hist + du[j], 1u);
     }
     if (tid == 0) s_carry = 0;
     __syncthreads();
+    tick(kProfFarScanned);  // --prof: histogram
     for (uint32_t base = 0; base <= maxd; base += T) {  // exclusive scan, T entries per step
       const uint32_t i = base + tid;
       const uint32_t x = i <= maxd ? hist[i] : 0u;
@@ -298,10 +308,25 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       if (tid == T - 1) s_carry = before + incl;
       __syncthreads();
     }
+    tick(kProfImprovements);  // --prof: scan
     // scatter into distance order, writing each vertex's sweep input at its
     // position: its slots u->v with d(v) > d(u) as (key d(u) + w + minw(v),
     // d(v) + 1), zero pairs pad.  One vertex per thread and step, every
     // load of a step in flight together (host: max degree <= kFlatMaxDeg).
+    uint32_t* const pos_of = w.q2 + off;  // sorted position per vertex (q2 is free after A)
+    for (uint32_t u0 = tid; u0 < n; u0 += T * kH) {
+      uint32_t du[kH], ps[kH];
+#pragma unroll
+      for (int j = 0; j < kH; ++j) du[j] = u0 + j * T < n ? __ldcg(dist + u0 + j * T) : kInfDist;
+#pragma unroll
+      for (int j = 0; j < kH; ++j) ps[j] = du[j] != kInfDist ? atomicAdd(hist + du[j], 1u) : 0u;
+#pragma unroll
+      for (int j = 0; j < kH; ++j)
+        if (du[j] != kInfDist) {
+          pos_of[u0 + j * T] = ps[j];
+          sorted_d[ps[j]] = du[j];
+        }
+    }
     constexpr int kU = 1;
     for (uint32_t u0 = tid; u0 < n; u0 += T * kU) {
       uint32_t du[kU], pos[kU], rb[kU], re[kU];
@@ -310,10 +335,12 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         const uint32_t u = u0 + j * T;
         du[j] = u < n ? __ldcg(dist + u) : kInfDist;
         rb[j] = re[j] = 0;
-        if (du[j] != kInfDist) row_of(u, rb[j], re[j]);
+        pos[j] = 0;
+        if (du[j] != kInfDist) {
+          row_of(u, rb[j], re[j]);
+          pos[j] = pos_of[u];
+        }
       }
-#pragma unroll
-      for (int j = 0; j < kU; ++j) pos[j] = du[j] != kInfDist ? atomicAdd(hist + du[j], 1u) : 0u;
       uint32_t v[kU][kFlatMaxDeg], wt[kU][kFlatMaxDeg], dv[kU][kFlatMaxDeg], mw[kU][kFlatMaxDeg];
 #pragma unroll
       for (int j = 0; j < kU; ++j)
@@ -334,7 +361,6 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         if (du[j] == kInfDist) continue;
-        sorted_d[pos[j]] = du[j];
         uint2* const out = ivl + static_cast<uint64_t>(pos[j]) * kE;
         int t = 0;
 #pragma unroll
