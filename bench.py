@@ -41,6 +41,8 @@ WORKLOADS = {
     "ba65536": dict(kind="ba", n=65536, mper=10, lo=1, hi=100, sources=None),
     "rmat20": dict(kind="rmat", scale=20, deg=32.0, lo=1, hi=255, sources=4096),
     "grid2048": dict(kind="grid", side=2048, lo=1, hi=1000, sources=1024),
+    # the 8-GPU config: 65,536 sources take ~8 min per step on one B200; the
+    # recorded one-GPU line (profiles/r01_bench_rmat24.json) uses --sources 592 --steps 2
     "rmat24": dict(kind="rmat", scale=24, deg=32.0, lo=1, hi=255, sources=65536),
     # small test workload (multi-rank checks), not a BASELINE config
     "rmat16": dict(kind="rmat", scale=16, deg=32.0, lo=1, hi=255, sources=512),
