@@ -17,7 +17,9 @@
 //      pile beyond it), distances only;
 //   B. DAG in-/out-degrees, reached count, max distance;
 //   C. sigma by a dependency-counted dataflow (a vertex is queued when its
-//      last predecessor is done: integer-valued fp64 sums, exact in any order);
+//      last predecessor is done: integer-valued fp64 sums, exact in any order;
+//      the hand-off is a CTA-scope acq_rel decrement, release store, acquire
+//      load);
 //   D. delta the same way in reverse, with the reference's term
 //      sigma[u] / sigma[v] * (1 + delta[v]) (engine.cpp:201) and node / edge BC;
 //   E. a counting sort of the distances, then one warp sweeps the thresholds
@@ -59,6 +61,21 @@ struct FlatWs {
 
 __device__ __forceinline__ uint32_t ld_vol(const uint32_t* a) { return *reinterpret_cast<const volatile uint32_t*>(a); }
 __device__ __forceinline__ void st_vol(uint32_t* a, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(a) = v; }
+// CTA-scope acquire load / release store / acq_rel decrement (the dataflow
+// hand-off: a vertex's sums are visible to whoever dequeues it)
+__device__ __forceinline__ uint32_t ld_acq(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(uint32_t* a, uint32_t v) {
+  asm volatile("st.release.cta.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t dec_acq_rel(uint32_t* a) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(0xFFFFFFFFu) : "memory");
+  return old;
+}
 
 template <int T, bool PACKED>
 __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p, const FlatWs w) {
@@ -480,19 +497,14 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         const uint32_t i = atomicAdd(&s_head, 1u);
         if (i >= reached) break;
         uint32_t u;
-        while ((u = ld_vol(qf + i)) == kFlatEmpty) __nanosleep(32);
-        __threadfence_block();
+        while ((u = ld_acq(qf + i)) == kFlatEmpty) __nanosleep(32);
         const double su = __ldcg(sigma + u);
         const uint32_t b = __ldg(g.offsets + u);
         for (uint32_t sm = __ldcg(flag + u) & 0xFFFFu; sm; sm &= sm - 1) {
           uint32_t v, wt;
           load_slot<PACKED>(g, b + __ffs(sm) - 1, v, wt);
           atomicAdd(sigma + v, su);
-          __threadfence_block();
-          if (atomicSub(npred + v, 1u) == 1u) {
-            __threadfence_block();
-            st_vol(qf + atomicAdd(&s_tail, 1u), v);
-          }
+          if (dec_acq_rel(npred + v) == 1u) st_rel(qf + atomicAdd(&s_tail, 1u), v);
         }
       }
       gsync();
@@ -511,8 +523,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         const uint32_t i = atomicAdd(&s_head, 1u);
         if (i >= reached) break;
         uint32_t v;
-        while ((v = ld_vol(qb + i)) == kFlatEmpty) __nanosleep(32);
-        __threadfence_block();
+        while ((v = ld_acq(qb + i)) == kFlatEmpty) __nanosleep(32);
         const double dvv = __ldcg(delta + v);
         const double sv = __ldcg(sigma + v);
         if (v != s) atomicAdd(p.node_bc + v, dvv);
@@ -525,11 +536,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           const double c = __ldcg(sigma + u) / sv * (1.0 + dvv);
           atomicAdd(delta + u, c);
           if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + x), c);
-          __threadfence_block();
-          if (atomicSub(nsucc + u, 1u) == 1u) {
-            __threadfence_block();
-            st_vol(qb + atomicAdd(&s_tail, 1u), u);
-          }
+          if (dec_acq_rel(nsucc + u) == 1u) st_rel(qb + atomicAdd(&s_tail, 1u), u);
         }
       }
     }
