@@ -192,48 +192,135 @@ class ClockSampler:
         return out
 
 
-def cpu_baseline(wl_name: str, wl: dict, target_s: float = 15.0):
-    """The compiled reference (oracle/_ref) bc_parallel on this host, bounded sample."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _rel_ok(a, b, rtol=1e-9):
+    """approx_rel of tests/conftest.py: |a-b| <= max(1e-12, rtol * max(|a|, |b|))."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    err = np.abs(a - b)
+    scale = np.maximum(np.abs(a), np.abs(b))
+    ok = err <= np.maximum(1e-12, rtol * scale)
+    rel = float(np.max(err / np.maximum(scale, 1e-300))) if len(a) else 0.0
+    return bool(ok.all()), rel
+
+
+def cpu_baseline(wl_name: str, wl: dict, g, src_all, gg, target_s: float = 10.0):
+    """The reference's CPU Brandes on this host, on bounded samples of the workload
+    (SURVEY.md §8(d)), plus the reference bench's score gate.
+
+    (i)  brandes_sequential (brandes.cpp:34-104, the paper's CPU baseline) as one
+         call per host core over disjoint source shards (a pure function,
+         brandes.hpp:22-24), and the same code on one core;
+    (ii) bc_parallel with the family's best strategy and workers = cores (not on
+         the grid: its O(n) threshold/settle scans per round make it infeasible).
+    Both run on the repo's CSR arrays handed to the reference library unchanged
+    (array-identical to the reference's build_csr: tests/test_host_graph.py).
+    The GPU's BC of each sample must match the reference's within 1e-9 relative
+    and bc_parallel's depth_per_source exactly (run_bench's verify,
+    bench.cpp:37-49,98-107; its own gate is 1e-6).  `value` is the faster of
+    (i) and (ii)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import REF_SO, Oracle, RefLib
+    import paper_1701_05975_b200 as W
+
     cores = os.cpu_count() or 1
-    if os.path.exists(REF_SO):
-        R = RefLib()
-        g, src_all = build_graph_ref(R, wl)
-        kind = "reference"
-        strategy = BEST_STRATEGY[wl["kind"]]
-        ref_step = ref_runner(R, g, wl["kind"], cores)
+    m = g.m
+    out = dict(unit="GTEPS", cores=cores, cpu_model=cpu_model())
+    gate = dict(rtol=1e-9, checks=[])
 
-        def run(src):
-            t = time.perf_counter()
-            ref_step(src)
-            return time.perf_counter() - t
-    else:  # port: the plain-C oracle, single-threaded
-        import paper_1701_05975_b200 as W  # graph arrays only; the timed code is the oracle
-        _, g, src_all = build_graph_ours(wl)
+    def gate_node(name, sample, ref_node, ref_depth=None):
+        r = gg.bc(W.EngineOptions(sources=np.asarray(sample, np.uint32)))
+        ok, rel = _rel_ok(r.node_bc, ref_node)
+        chk = dict(against=name, sources=int(len(sample)), node_bc_ok=ok, max_rel_err=rel)
+        if ref_depth is not None:
+            chk["depth_equal"] = bool(np.array_equal(r.depth_per_source, ref_depth))
+        gate["checks"].append(chk)
+
+    if not os.path.exists(REF_SO):  # port: the plain-C oracle, one thread
         O = Oracle()
-        kind = "port"
-        cores = 1
-        strategy = "eq4 (oracle)"
+        probe = src_all[:1]
+        t = time.perf_counter()
+        O.bc_eq4(g, sources=probe)
+        per = max(time.perf_counter() - t, 1e-9)
+        k = int(max(1, min(len(src_all), target_s / per)))
+        sample = src_all[:k]
+        t = time.perf_counter()
+        node, _, depth = O.bc_eq4(g, sources=sample)
+        t = time.perf_counter() - t
+        out.update(value=m * k / t / 1e9, cores=1, kind="port",
+                   sample=f"first {k} sources, oracle bc_eq4 single-thread, {t:.2f}s")
+        gate_node("oracle bc_eq4", sample, node, depth)
+        gate["passed"] = all(c["node_bc_ok"] for c in gate["checks"])
+        return out, gate
 
-        def run(src):
+    R = RefLib()
+    rg = R.csr_from_arrays(g)
+    try:
+        def brandes_shards(src):
+            shards = [s for s in np.array_split(np.asarray(src, np.uint32), cores) if len(s)]
             t = time.perf_counter()
-            O.bc_eq4(g, sources=src)
-            return time.perf_counter() - t
-    # calibrate on a small batch, then size the sample to ~target_s
-    probe = src_all[: max(1, min(len(src_all), cores))]
-    t_probe = run(probe)
-    per_src = t_probe / len(probe)
-    k = int(max(len(probe), min(len(src_all), target_s / max(per_src, 1e-9))))
-    k = max(k - k % max(1, min(cores, k)), len(probe)) if kind == "reference" else k
-    sample = src_all[:k]
-    t = run(sample)
-    value = g.m * len(sample) / t / 1e9
-    if kind == "reference":
-        R.free_csr(g)
-    return dict(value=value, unit="GTEPS", cores=cores, kind=kind,
-                sample=f"first {len(sample)} of the {wl_name} source list, {ref_label(wl['kind'], cores)}, "
-                       f"{t:.2f}s wall" if kind == "reference" else
-                       f"first {len(sample)} sources, oracle bc_eq4 single-thread, {t:.2f}s")
+            with ThreadPoolExecutor(len(shards)) as ex:  # ctypes releases the GIL
+                parts = list(ex.map(lambda sh: R.brandes(rg, sources=sh), shards))
+            return np.sum(parts, axis=0), time.perf_counter() - t
+
+        # (i) brandes_sequential x cores: probe with one source per core, then size to ~target_s
+        probe = src_all[: min(len(src_all), cores)]
+        node, t = brandes_shards(probe)
+        sample = probe
+        k = int(min(len(src_all), target_s * len(probe) / max(t, 1e-9)))
+        k -= k % cores
+        if k > len(probe):
+            sample = src_all[:k]
+            node, t = brandes_shards(sample)
+        bx = m * len(sample) / t / 1e9
+        out["brandes_sequential_x_cores"] = dict(value=bx, sources=int(len(sample)), seconds=round(t, 3),
+                                                 threads=cores)
+        gate_node("brandes_sequential", sample, node)
+        # the same code on one core, alone
+        t1 = time.perf_counter()
+        R.brandes(rg, sources=src_all[:1])
+        t1 = time.perf_counter() - t1
+        out["brandes_sequential_1core"] = dict(value=m / t1 / 1e9, sources=1, seconds=round(t1, 3))
+        best, best_desc = bx, f"brandes_sequential on {cores} threads over disjoint shards, {len(sample)} sources, {t:.2f}s"
+        # (ii) bc_parallel, best strategy, all cores
+        if wl["kind"] != "grid":
+            strategy = BEST_STRATEGY[wl["kind"]]
+            probe = src_all[: min(len(src_all), cores)]
+            t = time.perf_counter()
+            R.bc_parallel(rg, strategy, cores, sources=probe)
+            t = time.perf_counter() - t
+            k = int(min(len(src_all), target_s * len(probe) / max(t, 1e-9)))
+            k = max(len(probe), k - k % cores)
+            sample_p = src_all[:k]
+            t = time.perf_counter()
+            res = R.bc_parallel(rg, strategy, cores, sources=sample_p)
+            t = time.perf_counter() - t
+            bp = m * len(sample_p) / t / 1e9
+            out["bc_parallel"] = dict(value=bp, strategy=strategy, workers=cores, sources=int(len(sample_p)),
+                                      seconds=round(t, 3))
+            gate_node(f"bc_parallel {strategy}", sample_p, res["node_bc"], res["depth"])
+            if bp > best:
+                best, best_desc = bp, (f"bc_parallel strategy={strategy} workers={cores}, "
+                                       f"{len(sample_p)} sources, {t:.2f}s")
+        else:
+            out["bc_parallel"] = dict(value=None, note="DNF: O(n) threshold/settle scans per Eq. 4 round "
+                                                       "(~10^5 rounds per source, SURVEY.md §6)")
+    finally:
+        R.free_csr(rg)
+    out.update(value=best, kind="reference",
+               sample=f"{wl_name}: best reference CPU figure = {best_desc}; first sources of the workload's list")
+    gate["passed"] = all(c["node_bc_ok"] and c.get("depth_equal", True) for c in gate["checks"])
+    return out, gate
 
 
 def build_graph_ref(R, wl):
@@ -298,6 +385,61 @@ def run_reference_arm(args, wl_name, wl):
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this command under
+    torch.distributed.run with N ranks (one process per GPU, 127.0.0.1
+    rendezvous).  Fails loudly when fewer than N GPUs are visible (NCCL needs one
+    device per rank; --dist-backend gloo lets ranks share a device)."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if args.dist_backend == "nccl" and have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def shared_graph(wl, rank: int, world: int, barrier):
+    """Rank 0 builds the workload graph once; the other ranks map its arrays
+    from a per-run directory (/dev/shm when it has room) instead of
+    rebuilding it (R-MAT-24: ~77 s of host work per rank)."""
+    import shutil
+    from types import SimpleNamespace
+
+    t = time.perf_counter()
+    if world == 1:
+        _, g, src = build_graph_ours(wl)
+        return g, src, time.perf_counter() - t
+    run_id = os.environ.get("TORCHELASTIC_RUN_ID", "") + "_" + os.environ.get("MASTER_PORT", "0")
+    base = "/dev/shm"
+    if not os.path.isdir(base) or shutil.disk_usage(base).free < 24 << 30:
+        base = tempfile.gettempdir()
+    d = os.path.join(base, f"wbc_bench_{run_id}")
+    names = ("offsets", "adjacency", "weights", "min_incident_weight", "edge_id")
+    if rank == 0:
+        _, g, src = build_graph_ours(wl)
+        os.makedirs(d, exist_ok=True)
+        for nm in names:
+            np.save(os.path.join(d, nm + ".npy"), getattr(g, nm))
+        np.save(os.path.join(d, "sources.npy"), src)
+        with open(os.path.join(d, "dims.json"), "w") as f:
+            json.dump(dict(n=int(g.n), m=int(g.m)), f)
+    barrier()
+    if rank != 0:
+        with open(os.path.join(d, "dims.json")) as f:
+            dims = json.load(f)
+        g = SimpleNamespace(n=dims["n"], m=dims["m"],
+                            **{nm: np.load(os.path.join(d, nm + ".npy"), mmap_mode="r") for nm in names})
+        src = np.load(os.path.join(d, "sources.npy"))
+    return g, src, time.perf_counter() - t, d
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -307,8 +449,8 @@ def main():
     ap.add_argument("--workload", default="rmat20", choices=sorted(WORKLOADS))
     ap.add_argument("--sources", type=int, default=0, help="override the workload's source count")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-baseline-large", action="store_true",
-                    help="also time the reference on R-MAT-24 (its own generator + CSR build take ~10 min)")
+    ap.add_argument("--cpu-target-s", type=float, default=10.0,
+                    help="seconds of reference CPU work per baseline sample")
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--slots", type=int, default=0)
     ap.add_argument("--near", type=int, default=0)
@@ -321,6 +463,8 @@ def main():
         wl["sources"] = args.sources
     if args.impl == "reference":
         return run_reference_arm(args, args.workload, wl)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args)
 
     import torch
     import torch.distributed as dist
@@ -330,10 +474,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks", file=sys.stderr)
+    if args.dist_backend == "nccl" and world > torch.cuda.device_count():
+        print(f"bench.py: {world} NCCL ranks need {world} visible GPUs, found {torch.cuda.device_count()}",
+              file=sys.stderr)
+        return 2
     dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     if world > 1:
         if args.dist_backend == "nccl":
+            # NCCL prints its communicator (nranks, NVLS / NVLink transport) at init
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group("gloo")
@@ -347,10 +500,19 @@ def main():
             dist.all_reduce(c, op=op)
             t.copy_(c)
 
-    t_build = time.perf_counter()
-    _, g, src_all = build_graph_ours(wl)
-    t_build = time.perf_counter() - t_build
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    built = shared_graph(wl, rank, world, barrier)
+    g, src_all, t_build = built[:3]
     gg = W.GpuGraph(g, device=dev)
+    if world > 1:
+        barrier()  # every rank holds its replica: the shared arrays can go
+        if rank == 0:
+            import shutil
+            shutil.rmtree(built[3], ignore_errors=True)
     gg.set_tuning(args.threads, args.slots, args.near)
     shard = np.ascontiguousarray(src_all[rank::world])
     n, m = g.n, g.m
@@ -370,11 +532,6 @@ def main():
         if world > 1:
             all_reduce(d_node)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
     for _ in range(args.warmup):
         device_step()
     barrier()
@@ -386,12 +543,11 @@ def main():
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     t_start.record(stream)
-    launches = 0
     for i in range(args.steps):
         device_step(launch_events[i])
-        launches += gg.last_run_stats()["launches"]
     t_end.record(stream)
     barrier()
+    launches = args.steps * gg.last_run_stats()["launches"]  # every step issues the same launches
     clk = clocks.stop()
     elapsed = t_start.elapsed_time(t_end) / 1e3
     kernel_s = [a.elapsed_time(b) / 1e3 for a, b in launch_events]
@@ -429,6 +585,7 @@ def main():
     h2d = 4 * len(shard) + (8 * n if world > 1 else 0)
     d2h = 8 * n + 4 * n + 4 + (8 * n if world > 1 else 0)
 
+    rc = 0
     if rank == 0:
         peak, peak_src = load_peaks()
         per_launch_bytes = algorithmic_bytes_per_source(n, m) * len(shard)
@@ -444,34 +601,40 @@ def main():
                         peak_source=peak_src, kernel=gg.last_kernel(),
                         bytes_model="72m+88n per source (SURVEY.md 8d)",
                         launch_ms=round(avg_launch * 1e3, 3))
+        nccl = None
+        if world > 1 and args.dist_backend == "nccl":
+            v = torch.cuda.nccl.version()
+            nccl = dict(version=".".join(map(str, v)) if isinstance(v, tuple) else str(v), nranks=world,
+                        note="NCCL_DEBUG=INFO init lines (communicator, nRanks) precede this line")
         line = dict(metric=METRIC, value=round(value, 3), unit="GTEPS", n_gpus=world, steps=args.steps,
                     warmup=args.warmup, ms_per_step=round(elapsed / args.steps * 1e3, 3), higher_is_better=True,
                     scaling="strong", vs_baseline=None, dtype="u32 dist / f64 sigma,delta,BC", data="synthetic",
                     config=dict(workload=args.workload, graph=describe(wl), n=int(n), m=int(m),
                                 sources_per_step=int(total_sources), parallelism=f"source-partitioned x{world}",
                                 collective="none" if world == 1 else f"one {args.dist_backend} all_reduce of the partial BC",
+                                nccl=nccl,
                                 l2="inputs exceed L2 (CSR replica + per-source workspaces >> 126 MB), no flush",
                                 graph_build_s=round(t_build, 2)),
                     e2e=dict(value=round(e2e_value, 3), unit="GTEPS", h2d_bytes_per_step=int(h2d),
                              d2h_bytes_per_step=int(d2h), api="wbc_gpu_bc (host buffers)"),
                     roofline=roofline, clocks=clk, gpu_launches=int(launches),
                     run_stats=gg.last_run_stats(), bc_checksum=bc_sum)
-        if not args.no_cpu_baseline and world == 1 and args.workload == "rmat24" and not args.cpu_baseline_large:
-            line["cpu_baseline"] = dict(value=None, unit="GTEPS", cores=os.cpu_count(), kind="reference",
-                                        sample="skipped: the reference's own scale-24 generator and CSR build "
-                                               "take ~10 min on the host (--cpu-baseline-large runs it); "
-                                               "the rmat20 line carries the CPU ratio")
-        elif not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1:
             try:
-                line["cpu_baseline"] = cpu_baseline(args.workload, wl)
-            except Exception as ex:  # reported, never fatal
+                cb, gate = cpu_baseline(args.workload, wl, g, src_all, gg, args.cpu_target_s)
+                line["cpu_baseline"] = cb
+                line["score_gate"] = gate
+                if not gate["passed"]:
+                    print("bench.py: score gate FAILED: GPU BC differs from the reference CPU run", file=sys.stderr)
+                    rc = 3
+            except Exception as ex:  # the baseline is reported, its absence never fatal
                 line["cpu_baseline"] = dict(value=None, unit="GTEPS", cores=os.cpu_count(), kind="reference",
-                                            sample=f"failed: {ex}")
+                                            sample=f"failed: {ex!r}")
         print(json.dumps(line), flush=True)
     gg.close()
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return rc
 
 
 if __name__ == "__main__":

@@ -156,6 +156,17 @@ int wbc_gpu_profile_counters(wbc_gpu_graph* g, uint64_t* out16);
  * host-buffer runs only), [3]=kernel launches issued by the last call. */
 int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4);
 
+/* The last run's outcome, read from the device after synchronising it:
+ * [0]=slots used, [1]=threads per team, [2]=sources that overflowed the
+ * DAG-edge buffer, [3]=kernel launches, [4]=sources the distance-first
+ * kernel handed to the team kernel (0 on other launch shapes),
+ * [5]=1 when some shortest-path count sigma reached 2^53: sigma is an
+ * integer-valued fp64 count (engine.cpp:73-77) that is exact only below it,
+ * so BC from such a run may differ from the reference's.  Writes
+ * min(cap, WBC_RUN_INFO_FIELDS) entries. */
+#define WBC_RUN_INFO_FIELDS 6
+int wbc_gpu_last_run_info(wbc_gpu_graph* g, uint64_t* out, uint32_t cap);
+
 const char* wbc_gpu_last_error(void);
 
 /* ---- host-side helpers (the CSR loader and generators of the reference,

@@ -275,6 +275,22 @@ class RefLib:
         g.extra["handle"] = h
         return g
 
+    def csr_from_arrays(self, g) -> Csr:
+        """A reference CsrGraph holding the arrays of ``g`` (any object with the
+        CsrGraph fields): the repo's build_csr output is array-identical to the
+        reference's (tests/test_host_graph.py), so this skips the reference's
+        single-threaded build on large graphs."""
+        off, adj, eid = _u32(g.offsets), _u32(g.adjacency), _u32(g.edge_id)
+        w, minw = _f64(g.weights), _f64(g.min_incident_weight)
+        h = C.c_void_p()
+        self.lib.ref_csr_from_arrays.argtypes = [C.c_uint32, C.c_uint32] + [C.c_void_p] * 5 + [C.c_void_p]
+        self._check(self.lib.ref_csr_from_arrays(C.c_uint32(g.n), C.c_uint32(g.m), _ptr(off), _ptr(adj), _ptr(w),
+                                                 _ptr(eid), _ptr(minw), C.byref(h)))
+        out = Csr(g.n, g.m, off, adj, w, eid, minw, np.zeros(0, np.uint64), np.zeros(0, np.uint32),
+                  np.zeros(0, np.uint32))
+        out.extra["handle"] = h
+        return out
+
     def free_csr(self, g):
         h = g.extra.pop("handle", None)
         if h is not None:

@@ -123,6 +123,27 @@ int ref_csr_build(void* edges, void** out) {
   return guarded(
       [&] { *out = new wbc::CsrGraph(wbc::build_csr(*static_cast<wbc::EdgeList*>(edges))); });
 }
+// A CsrGraph filled from caller arrays (the repo's build_csr output, which
+// tests/test_host_graph.py proves array-identical to the reference's): lets
+// the CPU baseline skip the reference's single-threaded build at R-MAT-24.
+// original_id / edge_u / edge_v may be null (brandes_sequential never reads them).
+int ref_csr_from_arrays(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
+                        const double* weights, const uint32_t* edge_id, const double* min_incident_weight,
+                        void** out) {
+  return guarded([&] {
+    auto* g = new wbc::CsrGraph();
+    g->n = n;
+    g->m = m;
+    g->offsets.assign(offsets, offsets + uint64_t{n} + 1);
+    g->adjacency.assign(adjacency, adjacency + 2 * uint64_t{m});
+    g->weights.assign(weights, weights + 2 * uint64_t{m});
+    g->edge_id.assign(edge_id, edge_id + 2 * uint64_t{m});
+    g->min_incident_weight.assign(min_incident_weight, min_incident_weight + n);
+    g->original_id.resize(n);
+    for (uint32_t i = 0; i < n; ++i) g->original_id[i] = i;
+    *out = g;
+  });
+}
 void ref_csr_free(void* h) { delete static_cast<wbc::CsrGraph*>(h); }
 uint32_t ref_csr_n(void* h) { return static_cast<wbc::CsrGraph*>(h)->n; }
 uint32_t ref_csr_m(void* h) { return static_cast<wbc::CsrGraph*>(h)->m; }

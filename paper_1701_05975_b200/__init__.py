@@ -311,6 +311,9 @@ class BcResult:
     edge_bc: np.ndarray
     depth_per_source: np.ndarray
     elapsed: float = 0.0
+    # False when some shortest-path count reached 2^53 (sigma is exact below
+    # it, engine.cpp:73-77): BC may then differ from the reference's
+    sigma_exact: bool = True
 
 
 def _validate(opt: EngineOptions) -> None:
@@ -348,6 +351,16 @@ def _run_bc(fn, h, n: int, m: int, opt: Optional[EngineOptions]) -> BcResult:
     if rc:
         _raise(rc)
     return BcResult(node, edge, depth, el.value)
+
+
+def _run_info(h) -> dict:
+    """wbc_gpu_last_run_info: synchronises the graph's device, then reads the run's counters."""
+    st = np.zeros(6, np.uint64)
+    rc = L.load().wbc_gpu_last_run_info(h, _p(st), len(st))
+    if rc:
+        _raise(rc)
+    return dict(slots=int(st[0]), threads=int(st[1]), dag_overflow_sources=int(st[2]), launches=int(st[3]),
+                flat_fallback_sources=int(st[4]), sigma_overflow=bool(st[5]))
 
 
 def _csr_arrays(g: CsrGraph):
@@ -418,9 +431,8 @@ class GpuGraph:
         return {k: int(v) for k, v in zip(keys, out)}
 
     def last_run_stats(self) -> dict:
-        st = np.zeros(4, np.uint64)
-        L.load().wbc_gpu_last_run_stats(self._h, _p(st))
-        return dict(slots=int(st[0]), threads=int(st[1]), dag_overflow_sources=int(st[2]), launches=int(st[3]))
+        """Outcome of the last run (wbc_gpu_last_run_info; synchronises the device)."""
+        return _run_info(self._h)
 
     def last_kernel(self) -> str:
         buf = C.create_string_buffer(96)
@@ -429,7 +441,9 @@ class GpuGraph:
 
     def bc(self, opt: Optional[EngineOptions] = None) -> BcResult:
         """bc_parallel semantics on the resident graph (engine.cpp:372-457)."""
-        return _run_bc(L.load().wbc_gpu_bc, self._h, self.n, self.m, opt)
+        r = _run_bc(L.load().wbc_gpu_bc, self._h, self.n, self.m, opt)
+        r.sigma_exact = not _run_info(self._h)["sigma_overflow"]
+        return r
 
     def bc_device(self, d_sources_ptr: int, k: int, d_node_ptr: int, d_depth_ptr: int = 0,
                   d_edge_ptr: int = 0, halved: bool = False, edge_bc: bool = False, stream: int = 0) -> None:
@@ -544,7 +558,11 @@ class MultiGpuGraph:
                 _raise(rc)
 
     def bc(self, opt: Optional[EngineOptions] = None) -> BcResult:
-        return _run_bc(L.load().wbc_gpu_multi_bc, self._h, self.n, self.m, opt)
+        lib = L.load()
+        r = _run_bc(lib.wbc_gpu_multi_bc, self._h, self.n, self.m, opt)
+        r.sigma_exact = not any(_run_info(lib.wbc_gpu_multi_device_graph(self._h, i))["sigma_overflow"]
+                                for i in range(self.info()["num_devices"]))
+        return r
 
 def bc_parallel(g: CsrGraph, opt: Optional[EngineOptions] = None) -> BcResult:
     """Drop-in for wbc::bc_parallel (engine.hpp:122-130) running on the GPU."""

@@ -46,6 +46,7 @@ SIGNATURES = [
     ("wbc_gpu_set_profiling", i32, [vp, i32]),
     ("wbc_gpu_profile_counters", i32, [vp, vp]),
     ("wbc_gpu_last_run_stats", i32, [vp, vp]),
+    ("wbc_gpu_last_run_info", i32, [vp, vp, u32]),
     ("wbc_gpu_last_error", C.c_char_p, []),
     ("wbc_gpu_device_count", i32, [C.POINTER(i32)]),
     ("wbc_gpu_multi_create", i32, [u32, u32, vp, vp, vp, vp, vp, vp, i32, i32, C.POINTER(vp)]),

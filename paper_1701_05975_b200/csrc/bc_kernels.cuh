@@ -130,7 +130,8 @@ struct RunParams {
   double* edge_bc;         // null unless edge BC requested
   uint32_t* depth;         // null or n entries
   uint32_t near_width;     // S: width of the near window
-  unsigned int* overflow;  // count of sources that used the row-scan fallback
+  unsigned int* overflow;  // [0] count of sources that used the row-scan fallback,
+                           // [1] set when some sigma reached 2^53 (no longer exact)
   int keep_state;          // debug: write the shared-memory distances back (dump)
   const uint32_t* inv;     // original dense id -> device id (degree-descending relabel)
   uint32_t hot;            // device ids < hot keep their distance in shared memory
@@ -165,7 +166,7 @@ enum ProfCounter {
   kProfCyclesThreshold,
   kProfCyclesSettle,
   kProfCyclesBackward,
-  kProfAbortNear,   // bc_warp_kernel aborts, by cause
+  kProfAbortNear,   // reserved (kept for the counter block layout)
   kProfAbortFront,
   kProfAbortDag,
   kProfAbortDist,
@@ -198,6 +199,14 @@ struct DistView {
       gl[u] = v;
   }
 };
+
+// sigma is an integer-valued fp64 count (engine.cpp:73-77): exact in any
+// summation order while every partial sum stays below 2^53, i.e. while the
+// final value does.  A count at or above it is flagged (overflow[1]) so the
+// caller knows sigma-derived results may differ from the reference's.
+__device__ __forceinline__ void note_sigma(unsigned int* overflow, double s) {
+  if (s >= 9007199254740992.0) atomicOr(overflow + 1, 1u);
+}
 
 template <bool PACKED>
 __device__ __forceinline__ void load_slot(const GraphView& g, uint32_t e, uint32_t& u,
@@ -490,6 +499,7 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1536 / T)) bc_sources_kern
         if (tid < cnt) {
           const uint32_t v = sh.v[tid];
           sigma[v] = (v == s) ? 1.0 : sh.acc[tid];
+          note_sigma(p.overflow, sh.acc[tid]);
           delta[v] = 0.0;
         }
         __syncthreads();

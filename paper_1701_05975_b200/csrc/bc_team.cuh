@@ -697,7 +697,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
               const uint32_t dx = dist.load(x);
               if (dx != kInfDist && dx == dw + wt) {
                 hit = true;
-                c = __dmul_rn(__ddiv_rn(sw, __ldcg(sigma + x)), __dadd_rn(1.0, __ldcg(sdelta + x)));
+                const double sx = __ldcg(sigma + x);
+                note_sigma(p.overflow, sx);
+                c = __dmul_rn(__ddiv_rn(sw, sx), __dadd_rn(1.0, __ldcg(sdelta + x)));
                 if (eacc) eacc[__ldg(p.ref_edge_id + e)] = c;
               }
             }
@@ -736,7 +738,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             if (c + k * TT >= e) continue;
             const uint32_t v = d[k].y;
             // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
-            const double cc = __ldcg(sigma + u[k]) / __ldcg(sigma + v) * (1.0 + __ldcg(delta + v));
+            const double sv = __ldcg(sigma + v);
+            note_sigma(p.overflow, sv);
+            const double cc = __ldcg(sigma + u[k]) / sv * (1.0 + __ldcg(delta + v));
             atomicAdd(delta + u[k], cc);
             if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + d[k].x), cc);
           }
@@ -774,7 +778,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
               const uint32_t dx = dist.load(x);
               if (dx != kInfDist && dx == sh.dv[jl] + w) {
                 const uint32_t wv = sh.v[jl];
-                const double c2 = __ldcg(sigma + wv) / __ldcg(sigma + x) * (1.0 + __ldcg(delta + x));
+                const double sx = __ldcg(sigma + x);
+                note_sigma(p.overflow, sx);
+                const double c2 = __ldcg(sigma + wv) / sx * (1.0 + __ldcg(delta + x));
                 atomicAdd(&sh.acc[jl], c2);
                 if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + slot), c2);
               }

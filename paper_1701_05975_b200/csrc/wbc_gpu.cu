@@ -26,7 +26,6 @@
 #include "bc_flat.cuh"
 #include "bc_kernels.cuh"
 #include "bc_team.cuh"
-#include "bc_warp.cuh"
 #include "wbc_gpu.h"
 
 namespace {
@@ -86,7 +85,6 @@ int set_error(int code, const std::string& msg) { return ::set_error(code, msg);
 
 struct LaunchShape {
   uint32_t near_width = 0; // 0: the graph's automatic width
-  bool warp = false;       // bc_warp_kernel (one warp per source, team fallback)
   bool flat = false;       // bc_flat_kernel (CTA per source, distance-first; team fallback)
   int cluster = 0;         // 0: per-CTA kernel; else CTAs per team (team kernel, 1024 threads)
   int threads = 128;
@@ -129,12 +127,11 @@ struct wbc_gpu_graph {
   void* d_ws = nullptr;
   uint64_t ws_bytes = 0;
   wbc_dev::Workspace ws{};
-  // warp-kernel layout of the same allocation, and the team-kernel layout
-  // its aborted sources are re-run on
-  wbc_dev::WarpParams wl{};
+  // the team-kernel layout of the same allocation that the flat kernel's
+  // handed-back sources are re-run on
   wbc_dev::Workspace ws_fb{};
   int fb_slots = 0;
-  bool last_warp = false;     // the last run used bc_warp_kernel (layout wl / ws_fb)
+  bool last_flat = false;     // the last run used bc_flat_kernel
   int fill = 0;               // 2-CTA fill clusters beside a C >= 4 team launch
   // launch decisions are cached until a tuning knob changes
   uint64_t tune_gen = 1, shape_gen = 0, ws_gen = 0;
@@ -164,7 +161,6 @@ struct wbc_gpu_graph {
   int64_t tune_hot = -1;
   int64_t tune_l2hot = -1;
   bool tune_near = false;      // near_width set explicitly (else the launch shape may adjust it)
-  int tune_warp = 0;           // 1: bc_warp_kernel for flat graphs, 2: always (tests)
   int tune_flat = -1;          // -1 auto (flat, large graphs), 0 off, 1 wherever eligible
   uint32_t tune_flat_delta = 0;  // near-far window of bc_flat_kernel (0: max weight)
   uint32_t max_degree = 0, max_minw = 0;
@@ -264,7 +260,7 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   // take the distance-first kernel: grid-2048 x 1024 sources 2.98 s vs 5.4 s
   // for one-warp Eq. 4 teams, grid-512 2.93 vs 2.70 GTEPS; smaller graphs keep
   // the teams, which fit every source in flight (grid-128: 2.08 vs 0.52).
-  const bool auto_flat = g->tune_flat < 0 && g->tune_cluster < 0 && g->tune_warp == 0 && g->tune_threads == 0 &&
+  const bool auto_flat = g->tune_flat < 0 && g->tune_cluster < 0 && g->tune_threads == 0 &&
                          !g->skewed && g->n >= (1u << 18);
   if ((g->tune_flat > 0 || auto_flat) && flat_eligible(g)) {
     s.flat = true;
@@ -274,14 +270,6 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   }
   const uint64_t n = g->n;
   const bool tiny = n * 4 <= 24 * 1024;
-  const bool warp_ok = true;  // distances >= 2^31-1 abort to the team kernel at run time
-  if (g->tune_warp == 2 && warp_ok) {  // forced (tests)
-    s.cluster = 1;
-    s.threads = 32;
-    s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
-    s.warp = true;
-    return s;
-  }
   if (g->tune_cluster > 0) {
     s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
               : g->tune_cluster <= 8 ? 8 : 16;
@@ -319,10 +307,6 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
     s.cluster = 1;
     s.threads = 32;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
-    // the one-warp kernel with on-chip near set (bc_warp.cuh) is opt-in: it
-    // is instruction-latency-bound (~3K dependent warp instructions per
-    // round) and measured slower here (grid-2048: 1.03 vs 1.62 GTEPS)
-    s.warp = g->tune_warp != 0 && warp_ok;
     return s;
   }
   const void* fn = reinterpret_cast<const void*>(pick_kernel(s.threads, g->packed));
@@ -360,9 +344,9 @@ LaunchShape pick_shape(wbc_gpu_graph* g) {
 
 // Per-slot workspace bytes of each kernel family.
 uint64_t ws_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, 64); }
-uint64_t ws_dcap(const wbc_gpu_graph* g, bool warp) {
+uint64_t ws_dcap(const wbc_gpu_graph* g) {
   const uint64_t n = g->n;
-  return warp ? round_up(n + n / 8 + 1024, 64) : round_up(n + n / 2 + 1024, 64);
+  return round_up(n + n / 2 + 1024, 64);
 }
 uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
   return ws_ns(g) * (4 + 8 + 8 + 4 + 4 + 4 + 16 + 4 + 4 + 8 * uint64_t{std::max<uint32_t>(1, g->max_degree)});
@@ -395,17 +379,16 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   w.buckets = flat_buckets(g);
 }
 
-uint64_t ws_per_slot(const wbc_gpu_graph* g, bool warp, bool team, bool one_warp = false) {
+uint64_t ws_per_slot(const wbc_gpu_graph* g, bool team, bool one_warp = false) {
   const uint64_t ns = ws_ns(g);
-  if (warp) return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4) + ws_dcap(g, true) * 12;
   // one-warp teams compact their queues in place (a step reads its entries
   // before it writes, and writes never pass reads): no second buffers
-  return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? (one_warp ? 12 : 20) : 0)) + ws_dcap(g, false) * 8;
+  return ns * (4 + 8 + 8 + 4 + 4 + 4 + 4 + 4 + (team ? (one_warp ? 12 : 20) : 0)) + ws_dcap(g) * 8;
 }
 
 wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slots, bool team,
                                   bool one_warp = false) {
-  const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g, false);
+  const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g);
   auto carve = [&](uint64_t bytes) {
     char* q = p;
     p += bytes * slots;
@@ -433,27 +416,6 @@ wbc_dev::Workspace carve_cta_team(const wbc_gpu_graph* g, char* p, uint64_t slot
   return w;
 }
 
-void carve_warp(wbc_gpu_graph* g, char* p, uint64_t slots) {
-  const uint64_t ns = ws_ns(g), dag_cap = ws_dcap(g, true);
-  auto carve = [&](uint64_t bytes) {
-    char* q = p;
-    p += bytes * slots;
-    return q;
-  };
-  wbc_dev::WarpParams& w = g->wl;
-  w.n_stride = ns;
-  w.dag_cap = dag_cap;
-  w.sigma = reinterpret_cast<double*>(carve(ns * 8));
-  w.delta = reinterpret_cast<double*>(carve(ns * 8));
-  w.dag = reinterpret_cast<uint2*>(carve(dag_cap * 8));
-  w.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.level_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.dag_ends = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.far_q = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.dag_slot = reinterpret_cast<uint32_t*>(carve(dag_cap * 4));
-}
-
 int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
   if (g->d_ws && g->ws_bytes >= bytes) return WBC_OK;
   cudaFree(g->d_ws);
@@ -472,7 +434,7 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   // same knobs, same request, layout still carved: nothing to query or carve
-  const int shape_key = shape.cluster * 8192 + shape.threads * 4 + (shape.warp ? 1 : 0) + (shape.flat ? 2 : 0);
+  const int shape_key = shape.cluster * 8192 + shape.threads * 4 + (shape.flat ? 2 : 0);
   if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want && g->ws_shape_key == shape_key) {
     *slots_out = g->ws_slots_cached;
     return WBC_OK;
@@ -480,7 +442,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   g->ws_gen = 0;
   const bool team = shape.cluster > 0;
   const bool one_warp = team && shape.cluster == 1 && shape.threads <= 32;
-  const uint64_t per_slot = shape.flat ? ws_flat_per_slot(g) : ws_per_slot(g, shape.warp, team, one_warp);
+  const uint64_t per_slot = shape.flat ? ws_flat_per_slot(g) : ws_per_slot(g, team, one_warp);
   int slots = 0;
   if (shape.flat) {
     const void* f = reinterpret_cast<const void*>(g->packed ? wbc_dev::bc_flat_kernel<kFlatT, true>
@@ -496,21 +458,6 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(1, 32, g->packed, true)),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(wbc_dev::team_dyn_smem(32))));
-  } else if (shape.warp) {
-    for (const bool prof : {false, true}) {
-      const void* f = reinterpret_cast<const void*>(
-          g->packed ? (prof ? wbc_dev::bc_warp_kernel<true, true> : wbc_dev::bc_warp_kernel<true, false>)
-                    : (prof ? wbc_dev::bc_warp_kernel<false, true> : wbc_dev::bc_warp_kernel<false, false>));
-      WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sizeof(wbc_dev::WarpSmem))));
-    }
-    int per_sm = 0;
-    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, reinterpret_cast<const void*>(g->packed ? wbc_dev::bc_warp_kernel<true, false>
-                                                         : wbc_dev::bc_warp_kernel<false, false>),
-        32, sizeof(wbc_dev::WarpSmem)));
-    if (per_sm < 1) return set_error(WBC_E_CUDA, "warp kernel does not fit on an SM");
-    slots = per_sm * g->sm_count;
   }
   if (team) {
     for (const bool prof : {false, true}) {
@@ -520,7 +467,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
       WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(shape.dyn_smem)));
     }
-    if (!shape.warp) {
+    {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -543,7 +490,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
       if (clusters < 1) return set_error(WBC_E_CUDA, "team kernel: no cluster of this size fits");
       slots = clusters;
     }
-  } else if (!shape.warp && !shape.flat) {
+  } else if (!shape.flat) {
     const KernelFn fn = pick_kernel(shape.threads, g->packed);
     for (const bool prof : {false, true})
       WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_kernel(shape.threads, g->packed, prof)),
@@ -561,7 +508,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   // CTAs leave 36 of 148 SMs idle): a concurrent launch of 2-CTA clusters
   // fills them, sharing the source counter.
   int fill = 0;
-  if (team && !shape.warp && shape.cluster >= 4 && g->tune_fill && want > slots) {
+  if (team && shape.cluster >= 4 && g->tune_fill && want > slots) {
     fill = std::max(0, (g->sm_count - slots * shape.cluster) / 2);
     fill = std::min<int>(fill, want - slots);
     if (fill > 0)
@@ -582,27 +529,15 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   if (rc) return rc;
   *slots_out = slots;
   char* base = static_cast<char*>(g->d_ws);
-  g->last_warp = shape.warp;
+  g->last_flat = shape.flat;
   if (shape.flat) {
     // sources the flat kernel hands back run on one-warp teams over the same allocation
-    const uint64_t fb_per = ws_per_slot(g, false, true, true);
+    const uint64_t fb_per = ws_per_slot(g, true, true);
     if (g->ws_bytes < fb_per) {
       rc = ensure_bytes(g, fb_per);
       if (rc) return rc;
     }
     carve_flat(g, static_cast<char*>(g->d_ws), slots);
-    g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
-    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
-    g->ws_slots = slots;
-    g->ws_team = false;
-  } else if (shape.warp) {
-    // aborted sources re-run on one-warp teams over the same allocation
-    const uint64_t fb_per = ws_per_slot(g, false, true, true);
-    if (g->ws_bytes < fb_per) {
-      rc = ensure_bytes(g, fb_per);  // tiny workspaces: one fallback slot
-      if (rc) return rc;
-    }
-    carve_warp(g, static_cast<char*>(g->d_ws), slots);
     g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
     g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
     g->ws_slots = slots;
@@ -652,7 +587,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     shape.threads = 32;
     shape.dyn_smem = wbc_dev::team_dyn_smem(32);
   }
-  if (strict_lanes && (shape.cluster == 0 || shape.warp)) {
+  if (strict_lanes && shape.cluster == 0) {
     // strict merge runs on the team kernel (its row-scan backward)
     shape = LaunchShape{};
     shape.cluster = 1;
@@ -694,7 +629,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
                 : static_cast<uint32_t>(std::min<uint64_t>(g->n, (48ULL << 20) / 4 / std::max(1, slots)));
   p.prof = g->profiling ? g->d_prof : nullptr;
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter, 0, sizeof(unsigned long long), stream));
-  WBC_CUDA_TRY(cudaMemsetAsync(g->d_overflow, 0, sizeof(unsigned int), stream));
+  WBC_CUDA_TRY(cudaMemsetAsync(g->d_overflow, 0, 4 * sizeof(unsigned int), stream));
   WBC_CUDA_TRY(cudaMemsetAsync(g->d_node_dev, 0, uint64_t{g->n} * 8, stream));
   if (g->profiling)
     WBC_CUDA_TRY(cudaMemsetAsync(g->d_prof, 0, sizeof(unsigned long long) * wbc_dev::kProfCounters, stream));
@@ -734,51 +669,6 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     p.k_dev = g->d_abort_count;
     p.counter = g->d_counter2;
     p.hot = 0;
-    pick_team(1, 32, g->packed, g->profiling)<<<g->fb_slots, 32, wbc_dev::team_dyn_smem(32), stream>>>(p);
-    WBC_CUDA_TRY(cudaGetLastError());
-  } else if (shape.warp) {
-    if (g->abort_cap < k) {
-      cudaFree(g->d_abort_list);
-      cudaError_t e2 = cudaSuccess;
-      g->d_abort_list = dev_alloc<uint32_t>(k, e2);
-      if (e2 != cudaSuccess) {
-        g->abort_cap = 0;
-        return set_error(WBC_E_NOMEM, "abort list allocation failed");
-      }
-      g->abort_cap = k;
-    }
-    if (!g->d_abort_count) {
-      cudaError_t e2 = cudaSuccess;
-      g->d_abort_count = dev_alloc<unsigned long long>(2, e2);
-      if (e2 == cudaSuccess) g->d_counter2 = dev_alloc<unsigned long long>(1, e2);
-      if (e2 != cudaSuccess) return set_error(WBC_E_NOMEM, "counter allocation failed");
-    }
-    wbc_dev::WarpParams w = g->wl;
-    w.g = p.g;
-    w.sources = d_sources;
-    w.k = k;
-    w.counter = g->d_counter;
-    w.node_bc = g->d_node_dev;
-    w.edge_bc = p.edge_bc;
-    w.depth = d_depth;
-    w.near_width = p.near_width;
-    w.inv = g->d_inv;
-    w.abort_list = g->d_abort_list;
-    w.abort_count = g->d_abort_count;
-    w.prof = p.prof;
-    if (!edge_bc) w.dag_slot = nullptr;
-    WBC_CUDA_TRY(cudaMemsetAsync(g->d_abort_count, 0, sizeof(unsigned long long), stream));
-    WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter2, 0, sizeof(unsigned long long), stream));
-    const auto wk = g->packed ? (g->profiling ? wbc_dev::bc_warp_kernel<true, true> : wbc_dev::bc_warp_kernel<true, false>)
-                              : (g->profiling ? wbc_dev::bc_warp_kernel<false, true> : wbc_dev::bc_warp_kernel<false, false>);
-    wk<<<slots, 32, sizeof(wbc_dev::WarpSmem), stream>>>(w);
-    WBC_CUDA_TRY(cudaGetLastError());
-    // sources the warp kernel aborted: one-warp teams, count read on device
-    p.ws = g->ws_fb;
-    p.sources = g->d_abort_list;
-    p.k = k;
-    p.k_dev = g->d_abort_count;
-    p.counter = g->d_counter2;
     pick_team(1, 32, g->packed, g->profiling)<<<g->fb_slots, 32, wbc_dev::team_dyn_smem(32), stream>>>(p);
     WBC_CUDA_TRY(cudaGetLastError());
   } else if (shape.cluster > 0) {
@@ -827,11 +717,10 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   g->stats[0] = slots;
   g->stats[1] = shape.threads * std::max(1, shape.cluster);
   g->last_kernel = shape.flat ? std::string("bc_flat_kernel")
-                  : shape.warp ? std::string("bc_warp_kernel")
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  if (!strict_lanes) g->stats[3] = (shape.warp || shape.flat) ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
+  if (!strict_lanes) g->stats[3] = shape.flat ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
   return WBC_OK;
 }
 
@@ -905,8 +794,8 @@ int launch_strict(wbc_gpu_graph* g, const LaunchShape& shape, int slots, wbc_dev
   return WBC_OK;
 }
 
-// Slot-0 state of the last single-source run: the warp kernel's layout, or
-// the team layout its aborted source was re-run on.
+// Slot-0 state of the last single-source run (dumps run on the team or
+// per-CTA kernels, never on the flat kernel).
 struct Slot0 {
   uint32_t* dist;
   double* sigma;
@@ -915,25 +804,14 @@ struct Slot0 {
   uint32_t* level_ends;
   uint32_t* dag_ends;
   uint2* dag;
-  bool warp_dag;   // dag entries are (pred, succ) instead of (slot, succ)
-  bool masked;     // distances carry kSettledBit
+  bool pred_dag;   // dag entries are (pred, succ) instead of (slot, succ)
 };
 
 int slot0_state(wbc_gpu_graph* g, Slot0* out) {
   const wbc_dev::Workspace& w = g->ws;
   // team-kernel DAG records hold the predecessor (single-source runs never
   // compute edge BC); the per-CTA kernel records the slot
-  *out = Slot0{w.dist, w.sigma, w.delta, w.order, w.level_ends, w.dag_ends, w.dag, g->ws_team, false};
-  if (!g->last_warp) return WBC_OK;
-  unsigned long long aborted = 0;
-  WBC_CUDA_TRY(cudaMemcpy(&aborted, g->d_abort_count, 8, cudaMemcpyDeviceToHost));
-  if (aborted) {
-    const wbc_dev::Workspace& f = g->ws_fb;
-    *out = Slot0{f.dist, f.sigma, f.delta, f.order, f.level_ends, f.dag_ends, f.dag, true, false};
-  } else {
-    const wbc_dev::WarpParams& l = g->wl;
-    *out = Slot0{l.dist, l.sigma, l.delta, l.order, l.level_ends, l.dag_ends, l.dag, true, true};
-  }
+  *out = Slot0{w.dist, w.sigma, w.delta, w.order, w.level_ends, w.dag_ends, w.dag, g->ws_team};
   return WBC_OK;
 }
 
@@ -1141,7 +1019,7 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   if (err == cudaSuccess) g->d_inv = dev_alloc<uint32_t>(n, err);
   if (err == cudaSuccess) g->d_node_dev = dev_alloc<double>(n, err);
   if (err == cudaSuccess) g->d_counter = dev_alloc<unsigned long long>(1, err);
-  if (err == cudaSuccess) g->d_overflow = dev_alloc<unsigned int>(1, err);
+  if (err == cudaSuccess) g->d_overflow = dev_alloc<unsigned int>(4, err);
   if (err == cudaSuccess) g->d_prof = dev_alloc<unsigned long long>(wbc_dev::kProfCounters, err);
   if (err == cudaSuccess) {
     if (packed)
@@ -1253,7 +1131,6 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "hot") g->tune_hot = value;
   else if (k == "l2hot") g->tune_l2hot = value;
   else if (k == "cluster") g->tune_cluster = static_cast<int>(value);
-  else if (k == "warp") g->tune_warp = static_cast<int>(value);
   else if (k == "fill") g->tune_fill = static_cast<int>(value);
   else if (k == "flat") g->tune_flat = static_cast<int>(value);
   else if (k == "flat_delta") g->tune_flat_delta = static_cast<uint32_t>(std::max<int64_t>(0, value));
@@ -1282,6 +1159,21 @@ int wbc_gpu_profile_counters(wbc_gpu_graph* g, uint64_t* out16) {
 int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4) {
   if (!g || !stats4) return set_error(WBC_E_INVALID, "null argument");
   std::memcpy(stats4, g->stats, sizeof g->stats);
+  return WBC_OK;
+}
+
+int wbc_gpu_last_run_info(wbc_gpu_graph* g, uint64_t* out, uint32_t cap) {
+  if (!g || (!out && cap)) return set_error(WBC_E_INVALID, "null argument");
+  WBC_CUDA_TRY(cudaSetDevice(g->device));
+  WBC_CUDA_TRY(cudaDeviceSynchronize());  // the run's device-side counters are final
+  unsigned int ov[2] = {0, 0};
+  unsigned long long fb = 0;
+  if (g->stats[3]) {
+    WBC_CUDA_TRY(cudaMemcpy(ov, g->d_overflow, sizeof ov, cudaMemcpyDeviceToHost));
+    if (g->last_flat && g->d_abort_count) WBC_CUDA_TRY(cudaMemcpy(&fb, g->d_abort_count, 8, cudaMemcpyDeviceToHost));
+  }
+  const uint64_t v[WBC_RUN_INFO_FIELDS] = {g->stats[0], g->stats[1], ov[0], g->stats[3], fb, ov[1] ? 1u : 0u};
+  for (uint32_t i = 0; i < cap && i < WBC_RUN_INFO_FIELDS; ++i) out[i] = v[i];
   return WBC_OK;
 }
 
@@ -1407,7 +1299,7 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
     WBC_CUDA_TRY(cudaMemcpy(du.data(), st.dist, n * 4, cudaMemcpyDeviceToHost));
     if (dist)
       for (uint64_t i = 0; i < n; ++i) {
-        const uint32_t d = (st.masked && du[i] != wbc_dev::kInfDist) ? (du[i] & wbc_dev::kDistMask) : du[i];
+        const uint32_t d = du[i];
         dist[g->perm[i]] = d == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(d);
       }
     if (sigma) {
@@ -1449,7 +1341,7 @@ int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t
   if ((rc = slot0_state(g, &st))) return rc;
   std::vector<uint32_t> de(uint64_t{depth} + 1);
   WBC_CUDA_TRY(cudaMemcpy(de.data(), st.dag_ends, de.size() * 4, cudaMemcpyDeviceToHost));
-  const uint32_t len = std::min<uint64_t>(de[depth], st.warp_dag ? g->wl.dag_cap : g->ws.dag_cap);
+  const uint32_t len = std::min<uint64_t>(de[depth], g->ws.dag_cap);
   std::vector<uint2> d(len);
   if (len) WBC_CUDA_TRY(cudaMemcpy(d.data(), st.dag, uint64_t{len} * 8, cudaMemcpyDeviceToHost));
   std::vector<uint32_t> slots(g->packed ? 2ULL * g->m : 0);
@@ -1461,7 +1353,7 @@ int wbc_gpu_sssp_dag(wbc_gpu_graph* g, uint32_t source, uint32_t* pred, uint32_t
       WBC_CUDA_TRY(cudaMemcpy(slots64.data(), g->d_slots64, 16ULL * g->m, cudaMemcpyDeviceToHost));
   }
   for (uint32_t i = 0; i < len; ++i) {
-    const uint32_t u = st.warp_dag ? d[i].x : g->packed ? slots[d[i].x] >> g->wbits : slots64[d[i].x].x;
+    const uint32_t u = st.pred_dag ? d[i].x : g->packed ? slots[d[i].x] >> g->wbits : slots64[d[i].x].x;
     pred[i] = g->perm[u];
     succ[i] = g->perm[d[i].y];
   }

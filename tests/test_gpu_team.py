@@ -15,9 +15,8 @@ from test_gpu_parity import assert_close, check_graph
 
 pytestmark = pytest.mark.gpu
 
-# cluster size; "w" = one-warp teams (32-thread CTA per source); "k" = the
-# one-warp kernel with on-chip near set (bc_warp.cuh) and its team fallback
-CLUSTERS = (1, 2, 4, 8, 16, "w", "k")
+# cluster size; "w" = one-warp teams (32-thread CTA per source)
+CLUSTERS = (1, 2, 4, 8, 16, "w")
 
 
 def team_graph(W, g, c):
@@ -25,8 +24,6 @@ def team_graph(W, g, c):
     if c == "w":
         gg.set_param("cluster", 1)
         gg.set_param("threads", 32)
-    elif c == "k":
-        gg.set_param("warp", 2)
     else:
         gg.set_param("cluster", c)
     return gg
@@ -98,7 +95,7 @@ def test_team_hub_rows_and_sampled(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8, "w", "k"))
+@pytest.mark.parametrize("c", (1, 8, "w"))
 def test_team_dag_overflow_fallback(W, oracle, c):
     a = 60
     g = F.graph_of([(i, a + j, 1.0) for i in range(a) for j in range(a)])
@@ -119,7 +116,7 @@ def test_team_unpacked_slots(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (1, 8, "w", "k"))
+@pytest.mark.parametrize("c", (1, 8, "w"))
 def test_team_grid_large_diameter(W, oracle, c):
     el = W.assign_weights(W.gen_grid(64, 64), 1, 1000, 1)
     g = W.build_csr(el)
@@ -129,24 +126,12 @@ def test_team_grid_large_diameter(W, oracle, c):
     gg.close()
 
 
-def test_warp_kernel_aborts_fall_back(W, oracle):
-    """Hub rows give levels of thousands of vertices: the one-warp kernel
-    aborts those sources and the team kernel recomputes them (same stream)."""
-    el = W.assign_weights(W.gen_kronecker(12, 32.0, 4), 1, 255, 4)
-    g = W.build_csr(el)
-    gg = team_graph(W, g, "k")
-    src = W.sample_sources(g.n, 24, 3)
-    check_graph(W, oracle, g, gg=gg, sources=src, edge=True)
-    assert gg.last_kernel() == "bc_warp_kernel"
-    gg.close()
-
-
-def test_warp_kernel_grid_levels_and_dag(W, oracle):
-    """Large-diameter grid on the one-warp kernel: level sets and the
-    recorded DAG per level equal the oracle's Eq. 4 structure."""
+def test_one_warp_team_grid_levels_and_dag(W, oracle):
+    """Large-diameter grid on one-warp teams: level sets and the recorded DAG
+    per level equal the oracle's Eq. 4 structure."""
     el = W.assign_weights(W.gen_grid(48, 40), 1, 1000, 2)
     g = W.build_csr(el)
-    gg = team_graph(W, g, "k")
+    gg = team_graph(W, g, "w")
     off, adj, wt = g.offsets, g.adjacency, g.weights
     for s in (0, 777, g.n - 1):
         o = oracle.eq4_source(g, s)
@@ -164,10 +149,9 @@ def test_warp_kernel_grid_levels_and_dag(W, oracle):
     gg.close()
 
 
-def test_warp_kernel_distance_bound_aborts(W, oracle):
-    """Distances past 2^31 do not fit beside the settled bit: the one-warp
-    kernel aborts and the team kernel (u32 distances) finishes the source."""
+def test_one_warp_team_large_distances(W, oracle):
+    """Distances past 2^31 (u32 distances, n * max_w < 2^32) on one-warp teams."""
     g = F.graph_of([(i, i + 1, 30_000_000.0) for i in range(99)])  # path: d reaches 2.97e9
-    gg = team_graph(W, g, "k")
+    gg = team_graph(W, g, "w")
     check_graph(W, oracle, g, gg=gg, sources=[0, 5, 99], edge=True)
     gg.close()

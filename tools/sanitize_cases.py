@@ -21,8 +21,6 @@ cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("team C=2", kron, {"cluster": 2}),
          ("team C=4", kron, {"cluster": 4}),
          ("one-warp team", grid, {"cluster": 1, "threads": 32}),
-         ("warp kernel + fallback", kron, {"warp": 2}),
-         ("warp kernel", grid, {"warp": 2}),
          ("flat kernel", grid, {"flat": 1}),
          ("flat kernel + team fallback", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
          ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8})]
