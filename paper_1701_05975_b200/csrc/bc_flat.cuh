@@ -1,89 +1,175 @@
 // bc_flat.cuh -- per-source pipeline for flat, large-diameter graphs (grid /
-// road-like: small degrees, ~10^5 Eq. 4 rounds per source).
+// road-like: degree <= 8, ~10^5 Eq. 4 rounds per source).
 //
 // The Eq. 4 round process (engine.cpp:144-222) is inherently sequential: one
-// round settles ~45 vertices of a 2048^2 grid, and the team kernel spends
-// ~50K cycles of dependent memory round trips on each (profiles/
+// round settles ~45 vertices of a 2048^2 grid, and a round-by-round kernel
+// spends ~50K cycles of dependent memory round trips on each (profiles/
 // r01_ncu_team_grid2048.md).  This kernel takes the rounds off the critical
 // path.  Everything the result needs is a function of the final distances
 // (tests/test_depth_theory.py):
-//   * sigma / delta need only the shortest-path DAG, in any topological order;
+//   * sigma / delta need only the shortest-path DAG, in any topological
+//     order -- distance order is one;
 //   * the Eq. 4 levels are S_{r+1} = {v : d(v) < D_r} with
 //     D_r = min over slots u->v, d(u) < D_{r-1} <= d(v), of d(u) + w + minw(v),
 //     so depth_per_source is one monotone sweep over the distance-sorted
 //     vertices.
-// One CTA per source runs:
-//   A. near-far SSSP (Bellman-Ford inside a window of width `delta`, a far
-//      pile beyond it), distances only;
-//   B. DAG in-/out-degrees, reached count, max distance;
-//   C. sigma by a dependency-counted dataflow (a vertex is queued when its
-//      last predecessor is done: integer-valued fp64 sums, exact in any order;
-//      the hand-off is a CTA-scope acq_rel decrement, release store, acquire
-//      load);
-//   D. delta the same way in reverse, with the reference's term
-//      sigma[u] / sigma[v] * (1 + delta[v]) (engine.cpp:201) and node / edge BC;
-//   E. a counting sort of the distances, then one warp sweeps the thresholds
-//      with a shared-memory bucket array (key -> largest successor distance),
-//      concurrently with C and D on the other warps.
-// Sources whose distances exceed the counting-sort range are handed to the
-// team kernel (abort list), before anything is accumulated.
+//
+// One CTA per source.  The graph is read through an ELL copy of its rows:
+// one record per vertex (KE packed slots and KE sweep keys, 32 B for KE = 4,
+// so one sector), no offsets lookup.  The only vertex-indexed state is one
+// 8-byte word per vertex, (distance, sorted position); everything else lives
+// in distance order, where the pull passes below touch it coalesced or
+// within a few thousand positions of the current one (L2-resident):
+//   A. near-far SSSP, distances only: Bellman-Ford inside a window
+//      [lo, lo + delta) of width `delta_w`, a far pile beyond it.  A vertex
+//      joins the window's member list exactly once, when its distance first
+//      drops below the window end (the atomicMin that sees the crossing, or
+//      the far refill).  When a window closes its members are final; a
+//      shared-memory counting sort on d - lo appends them to `order` /
+//      `ord_d` and writes each one's position into its word, so the whole
+//      source ends up sorted by distance with no pass over n.
+//   B. sigma, pulled in distance order (thread per position): a vertex sums
+//      sigma over its DAG predecessors (d(u) + w == d(v)), all at earlier
+//      positions, waiting on each until it is nonzero (sigma >= 1 once
+//      written: the value is its own completion flag).  Integer-valued fp64,
+//      exact in any order below 2^53 (engine.cpp:73-77).  The same pass
+//      writes, per position, the successor mask and successor positions, and
+//      the threshold-sweep entries of every slot to a farther neighbour
+//      (w + minw(v), d(v) - d(u)), all coalesced.
+//   C. delta, pulled in reverse distance order by all warps but warp 0:
+//      c = sigma(u) * coef(v) over DAG successors v, where
+//      coef(v) = (1 + delta(v)) / sigma(v) is written once v is final
+//      (positive: its own completion flag); the reference's term is
+//      sigma[u] / sigma[v] * (1 + delta[v]) (engine.cpp:201), equal up to
+//      fp64 rounding.  Node BC += delta (u != s), edge BC += c.
+//      Concurrently warp 0 sweeps the Eq. 4 thresholds: a shared-memory
+//      bucket ring keyed by d(u) + w + minw(v) holds the largest successor
+//      distance + 1 (a key is live while that is above the threshold); the
+//      sorted distances and entries stream through a cp.async ring of
+//      shared-memory chunks, so a round costs shared-memory work only.
+// No source is ever handed back: the window sort's range is delta_w, not the
+// distance range.
 #pragma once
 
 #include "bc_kernels.cuh"
 
 namespace wbc_dev {
 
-constexpr uint32_t kFlatEmpty = 0xFFFFFFFFu;
-constexpr int kFlatMaxDeg = 8;        // interval slots per vertex in the sweep input
+constexpr int kFlatMaxDeg = 8;        // ELL row width: 4 or 8 slots
 constexpr int kFlatBuckets = 16384;   // shared-memory keys: maxw + max minw + 2 must fit
+constexpr int kFlatChunk = 256;       // sweep ring: positions per chunk
+constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in flight)
 
 struct FlatWs {
-  uint64_t n_stride;
-  uint32_t* dist;
-  double* sigma;
-  double* delta;
-  uint32_t* npred;
-  uint32_t* nsucc;
-  uint32_t* flag;
-  uint32_t* q0;
+  uint64_t n_stride;        // multiple of kFlatChunk
+  uint2* dp;                // by vertex: (distance, sorted position)
+  uint32_t* order;          // by position: vertex in distance order
+  uint32_t* ord_d;          // by position: its distance
+  uint32_t* mem;            // the open window's members (unsorted)
+  uint32_t* q0;             // near / next near / far / next far queues
   uint32_t* q1;
   uint32_t* q2;
   uint32_t* q3;
-  uint32_t* hist;      // n_stride entries: the counting-sort range of distances
-  uint32_t* sorted_d;  // their distances
-  uint2* ivl;          // per sorted position, ivl_stride (key, successor distance + 1) pairs
-  uint32_t ivl_stride; // the graph's max degree (<= kFlatMaxDeg)
-  uint32_t delta_w;    // near-far window width
-  uint32_t buckets;    // power of two >= maxw + max minw + 2
-  uint32_t* abort_list;
-  unsigned long long* abort_count;
+  double* psig;             // by position: sigma, 0 until final
+  double* pcoef;            // by position: (1 + delta) / sigma, 0 until final
+  uint32_t* pinfo;          // by position: successor mask | predecessor mask << 8
+  uint32_t* psucc;          // by position: KE neighbour positions (successor slots only)
+  uint32_t* ent;            // by position: KE sweep entries (w + minw(v)) | (d(v) - d(u)) << 16, 0 = none
+  const uint32_t* ell;      // n x 2KE words: KE slots (neighbour << wbits | weight, weight 0 = empty),
+                            // KE u16 keys weight + minw(neighbour), padding to a 32-byte multiple
+  const uint32_t* ell_eid;  // n x KE canonical edge ids (edge BC)
+  uint32_t delta_w;         // window width (<= kFlatBuckets)
+  uint32_t buckets;         // power of two >= maxw + max minw + 2
+  uint32_t hist_words;      // shared-memory words before the sweep ring: max(buckets, delta_w)
 };
 
-__device__ __forceinline__ uint32_t ld_vol(const uint32_t* a) { return *reinterpret_cast<const volatile uint32_t*>(a); }
-__device__ __forceinline__ void st_vol(uint32_t* a, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(a) = v; }
-// CTA-scope acquire load / release store / acq_rel decrement (the dataflow
-// hand-off: a vertex's sums are visible to whoever dequeues it)
-__device__ __forceinline__ uint32_t ld_acq(const uint32_t* a) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+__device__ __forceinline__ double ld_relaxed_f64(const double* a) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_rel(uint32_t* a, uint32_t v) {
-  asm volatile("st.release.cta.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_f64(double* a, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t dec_acq_rel(uint32_t* a) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(0xFFFFFFFFu) : "memory");
-  return old;
+// spin until a completion-flag value (nonzero) appears
+__device__ __forceinline__ double wait_nonzero(const double* a) {
+  double v = ld_relaxed_f64(a);
+  while (v == 0.0) {
+    __nanosleep(64);
+    v = ld_relaxed_f64(a);
+  }
+  return v;
+}
+// barrier `id` over `count` threads that also ORs a predicate across them
+__device__ __forceinline__ int bar_or(uint32_t pred, int id, int count) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(pred), "r"(id), "r"(count)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int T, bool PACKED>
+// Dynamic shared memory of bc_flat_kernel<T, KE>.
+inline size_t flat_dyn_smem(uint32_t hist_words, int ke) {
+  return (static_cast<size_t>(hist_words) + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke)) * 4;
+}
+
+// ELL record of v: 2 KE words (slots, then keys two per word)
+template <int KE>
+__device__ __forceinline__ const uint4* ell_rec(const FlatWs& w, uint32_t v) {
+  return reinterpret_cast<const uint4*>(w.ell + static_cast<uint64_t>(v) * (2 * KE));
+}
+template <int KE>
+__device__ __forceinline__ void ell_row(const FlatWs& w, uint32_t v, uint32_t (&r)[KE]) {
+  const uint4* p = ell_rec<KE>(w, v);
+#pragma unroll
+  for (int q = 0; q < KE / 4; ++q) {
+    const uint4 x = __ldg(p + q);
+    r[4 * q] = x.x;
+    r[4 * q + 1] = x.y;
+    r[4 * q + 2] = x.z;
+    r[4 * q + 3] = x.w;
+  }
+}
+template <int KE>
+__device__ __forceinline__ void ell_keys(const FlatWs& w, uint32_t v, uint32_t (&k)[KE]) {
+  const uint4* p = ell_rec<KE>(w, v) + KE / 4;
+  if constexpr (KE == 4) {
+    const uint2 x = __ldg(reinterpret_cast<const uint2*>(p));
+    k[0] = x.x & 0xFFFFu;
+    k[1] = x.x >> 16;
+    k[2] = x.y & 0xFFFFu;
+    k[3] = x.y >> 16;
+  } else {
+    const uint4 x = __ldg(p);
+    const uint32_t a[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      k[2 * i] = a[i] & 0xFFFFu;
+      k[2 * i + 1] = a[i] >> 16;
+    }
+  }
+}
+__device__ __forceinline__ uint32_t* dist_of(uint2* dp, uint32_t v) { return reinterpret_cast<uint32_t*>(dp + v); }
+
+template <int T, int KE>
 __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p, const FlatWs w) {
-  // p.prof: per-phase SM cycles of thread 0, reusing the team kernel's counter
-  // slots: init -> kProfCyclesInit, A -> kProfCyclesRelax, B ->
-  // kProfCyclesThreshold, E1 histogram -> kProfFarScanned, scan ->
-  // kProfImprovements, scatter + sweep input -> kProfNearScanned, E2 || C/D ->
-  // kProfRefills; A's phases -> kProfRounds
+  static_assert(KE == 4 || KE == 8, "ELL row width");
+  // p.prof: per-phase SM cycles of thread 0 (init -> kProfCyclesInit, A ->
+  // kProfCyclesRelax, B -> kProfCyclesThreshold, C -> kProfCyclesBackward),
+  // A's barrier phases -> kProfRounds, windows -> kProfRefills
   unsigned long long t_last = 0;
   auto tick = [&](int slot) {
     if (p.prof && threadIdx.x == 0) {
@@ -93,347 +179,359 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     }
   };
   __shared__ unsigned long long s_src;
-  __shared__ uint32_t s_ring[3][4];  // per-phase counters: [append a, append b, min, spare]
-  __shared__ uint32_t s_reached, s_maxd, s_head, s_tail, s_carry;
+  __shared__ uint32_t s_ring[3][4];  // per-phase counters: [near, far, members, far min]
   __shared__ uint32_t s_warp[T / 32];
-  extern __shared__ uint32_t bucket[];  // w.buckets entries (dynamic)
+  constexpr int kU = 2;                  // positions per thread in a pull block
+  constexpr uint32_t kBlkB = T * kU;     // pass B block (all threads)
+  constexpr uint32_t kBlkC = (T - 32) * kU;  // pass C block (warps 1..)
+  __shared__ double s_blk[kBlkB];        // the block's sigma (B) / coef (C); 0 = not final
+  volatile double* const s_blk_v = s_blk;
+  extern __shared__ uint32_t smem[];  // [hist_words] hist / buckets, then the sweep ring
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31, wid = tid >> 5;
   const uint64_t off = static_cast<uint64_t>(blockIdx.x) * w.n_stride;
-  uint32_t* const dist = w.dist + off;
-  double* const sigma = w.sigma + off;
-  double* const delta = w.delta + off;
-  uint32_t* const npred = w.npred + off;
-  uint32_t* const nsucc = w.nsucc + off;
-  uint32_t* const flag = w.flag + off;
-  uint32_t* const hist = w.hist + off;
-  uint32_t* const sorted_d = w.sorted_d + off;
-  const uint32_t kE = w.ivl_stride;
-  uint2* const ivl = w.ivl + off * kE;
-  const uint32_t n = g.n;
-  const unsigned long long k_total = p.k_dev ? __ldcg(p.k_dev) : p.k;
-  auto row_of = [&](uint32_t v, uint32_t& b, uint32_t& e) {
-    b = __ldg(g.offsets + v);
-    e = __ldg(g.offsets + v + 1);
-  };
+  uint2* const dp = w.dp + off;
+  uint32_t* const order = w.order + off;
+  uint32_t* const ord_d = w.ord_d + off;
+  uint32_t* const mem = w.mem + off;
+  double* const psig = w.psig + off;
+  double* const pcoef = w.pcoef + off;
+  uint32_t* const pinfo = w.pinfo + off;
+  uint32_t* const psucc = w.psucc + off * KE;
+  uint32_t* const ent = w.ent + off * KE;
+  uint32_t* const hist = smem;
+  const uint32_t wbits = g.wbits, wmask = g.wmask;
 
   for (;;) {
     if (tid == 0) s_src = atomicAdd(p.counter, 1ULL);
     __syncthreads();
     const unsigned long long idx = s_src;
-    if (idx >= k_total) break;
+    if (idx >= p.k) break;
     const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(p.src_base + idx);
     const uint32_t s = __ldg(p.inv + s_orig);
     tick(-1);
 
-    // ---- init
-    for (uint32_t i = tid; i < n; i += T) {
-      dist[i] = i == s ? 0u : kInfDist;
-      sigma[i] = 0.0;
-      delta[i] = 0.0;
-      npred[i] = 0;
-      flag[i] = 0;
+    // ---- init: every word (infinite distance, position 0)
+    {
+      uint4* const d4 = reinterpret_cast<uint4*>(dp);
+      const uint32_t n2 = static_cast<uint32_t>(w.n_stride / 2);
+      for (uint32_t i = tid; i < n2; i += T) __stcg(d4 + i, make_uint4(kInfDist, 0u, kInfDist, 0u));
     }
-    if (tid < 12) (&s_ring[0][0])[tid] = tid % 4 == 2 ? kInfDist : 0u;
-    if (tid == 0) w.q0[off] = s;
+    if (tid < 12) (&s_ring[0][0])[tid] = tid % 4 == 3 ? kInfDist : 0u;
+    __syncthreads();
+    if (tid == 0) {
+      *dist_of(dp, s) = 0;
+      w.q0[off] = s;
+      mem[0] = s;
+    }
     __syncthreads();
     tick(kProfCyclesInit);
 
-    // ---- A. near-far SSSP
+    // ---- A. near-far SSSP; windows sorted into `order` as they close
     uint32_t* nq = w.q0 + off;
     uint32_t* nn = w.q1 + off;
     uint32_t* fq = w.q2 + off;
     uint32_t* fq2 = w.q3 + off;
-    uint32_t near_len = 1, far_len = 0, iter = 1, ph = 0;
-    uint64_t thr = w.delta_w;
+    uint32_t near_len = 1, far_len = 0, mem_len = 1, olen = 0, ph = 0, windows = 0;
+    uint64_t lo = 0, thr = w.delta_w;
     for (;;) {
       uint32_t* R = s_ring[ph % 3];
       if (tid == 0) {
         uint32_t* Z = s_ring[(ph + 1) % 3];
         Z[0] = 0;
         Z[1] = 0;
-        Z[2] = kInfDist;
+        Z[2] = 0;
+        Z[3] = kInfDist;
       }
       const uint32_t thr32 = thr >= kInfDist ? kInfDist : static_cast<uint32_t>(thr);
       if (near_len) {
-        // relax every near vertex (thread per vertex: flat rows are short)
-        // (the row's slot words, then its distance gathers, then its atomics:
-        // each stage's loads are in flight together)
+        // relax every near vertex: its ELL slots, then the neighbours'
+        // distances, then the atomics (each stage's loads in flight together)
         for (uint32_t i = tid; i < near_len; i += T) {
           const uint32_t v = nq[i];
-          const uint32_t dv = __ldcg(dist + v);
-          uint32_t b, e;
-          row_of(v, b, e);
-          uint32_t us[kFlatMaxDeg], nd[kFlatMaxDeg], old[kFlatMaxDeg];
+          const uint32_t dv = __ldcg(dist_of(dp, v));
+          uint32_t r[KE], u[KE], nd[KE], old[KE];
+          ell_row<KE>(w, v, r);
 #pragma unroll
-          for (int x = 0; x < kFlatMaxDeg; ++x) {
-            us[x] = kFlatEmpty;
-            nd[x] = kInfDist;
-            if (b + x < e) {
-              uint32_t wt;
-              load_slot<PACKED>(g, b + x, us[x], wt);
-              nd[x] = dv + wt;
-            }
+          for (int x = 0; x < KE; ++x) {
+            const uint32_t wt = r[x] & wmask;
+            u[x] = r[x] >> wbits;
+            nd[x] = wt ? dv + wt : kInfDist;
           }
 #pragma unroll
-          for (int x = 0; x < kFlatMaxDeg; ++x)
-            if (us[x] != kFlatEmpty && nd[x] >= __ldcg(dist + us[x])) us[x] = kFlatEmpty;
+          for (int x = 0; x < KE; ++x)
+            if (nd[x] != kInfDist && nd[x] >= __ldcg(dist_of(dp, u[x]))) nd[x] = kInfDist;
 #pragma unroll
-          for (int x = 0; x < kFlatMaxDeg; ++x) old[x] = us[x] != kFlatEmpty ? atomicMin(dist + us[x], nd[x]) : 0u;
+          for (int x = 0; x < KE; ++x) old[x] = nd[x] != kInfDist ? atomicMin(dist_of(dp, u[x]), nd[x]) : 0u;
 #pragma unroll
-          for (int x = 0; x < kFlatMaxDeg; ++x) {
-            if (us[x] == kFlatEmpty || nd[x] >= old[x]) continue;
-            const uint32_t u = us[x];
+          for (int x = 0; x < KE; ++x) {
+            if (nd[x] == kInfDist || nd[x] >= old[x]) continue;
             if (nd[x] < thr32) {
-              if (atomicExch(flag + u, iter + 1) != iter + 1) nn[atomicAdd(&R[0], 1u)] = u;
+              // duplicates in the next near list are harmless (a re-relax
+              // reads the current distance); members are appended once, at
+              // the crossing below the window end
+              nn[atomicAdd(&R[0], 1u)] = u[x];
+              if (old[x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u[x];
             } else if (old[x] == kInfDist) {
-              fq[far_len + atomicAdd(&R[1], 1u)] = u;
+              fq[far_len + atomicAdd(&R[1], 1u)] = u[x];
             }
           }
         }
         __syncthreads();
         near_len = R[0];
         far_len += R[1];
+        mem_len += R[2];
         uint32_t* t = nq;
         nq = nn;
         nn = t;
-        ++iter;
         ++ph;
         continue;
       }
+      // the window [lo, thr) is closed: its members are final.  Counting
+      // sort on d - lo (< delta_w) appends them to order / ord_d and records
+      // each one's position; its sigma flag is cleared for pass B.
+      if (mem_len) {
+        const uint32_t span = static_cast<uint32_t>(thr - lo < w.delta_w ? thr - lo : w.delta_w);
+        for (uint32_t i = tid; i < span; i += T) hist[i] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < mem_len; i += T) atomicAdd(hist + (__ldcg(dist_of(dp, mem[i])) - lo), 1u);
+        __syncthreads();
+        // exclusive scan of hist[0, span): a contiguous chunk per thread
+        const uint32_t per = (span + T - 1) / T, b0 = min(span, tid * per), b1 = min(span, b0 + per);
+        uint32_t loc = 0;
+        for (uint32_t i = b0; i < b1; ++i) loc += hist[i];
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        if (lane == 31) s_warp[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+          uint32_t ws = lane < T / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= static_cast<uint32_t>(o)) ws += y;
+          }
+          if (lane < T / 32) s_warp[lane] = ws;
+        }
+        __syncthreads();
+        uint32_t run = olen + (wid ? s_warp[wid - 1] : 0u) + incl - loc;
+        for (uint32_t i = b0; i < b1; ++i) {
+          const uint32_t c = hist[i];
+          hist[i] = run;
+          run += c;
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < mem_len; i += T) {
+          const uint32_t u = mem[i];
+          const uint32_t du = __ldcg(dist_of(dp, u));
+          const uint32_t q = atomicAdd(hist + (du - lo), 1u);
+          order[q] = u;
+          ord_d[q] = du;
+          dp[u].y = q;
+          __stcg(psig + q, 0.0);
+        }
+        olen += mem_len;
+        mem_len = 0;
+        ++windows;
+        __syncthreads();
+      }
       if (far_len == 0) break;
-      // refill: far entries inside the next window become near; the rest are
-      // compacted into the other far buffer
+      // next window [thr, thr + delta): far entries inside it become near
+      // (and members); the rest are compacted into the other far buffer
       const uint64_t thr_new = thr + w.delta_w;
       const uint32_t tn32 = thr_new >= kInfDist ? kInfDist : static_cast<uint32_t>(thr_new);
       for (uint32_t i = tid; i < far_len; i += T) {
         const uint32_t u = fq[i];
-        const uint32_t du = __ldcg(dist + u);
-        if (du < thr32) continue;  // reached the near window earlier: relaxed already
+        const uint32_t du = __ldcg(dist_of(dp, u));
+        if (du < thr32) continue;  // joined an earlier window: sorted already
         if (du < tn32) {
-          if (atomicExch(flag + u, iter + 1) != iter + 1) nq[atomicAdd(&R[0], 1u)] = u;
+          nq[atomicAdd(&R[0], 1u)] = u;
+          mem[atomicAdd(&R[2], 1u)] = u;
         } else {
           fq2[atomicAdd(&R[1], 1u)] = u;
-          atomicMin(&R[2], du);
+          atomicMin(&R[3], du);
         }
       }
       __syncthreads();
       near_len = R[0];
       far_len = R[1];
+      mem_len = R[2];
       {
         uint32_t* t = fq;
         fq = fq2;
         fq2 = t;
       }
+      lo = thr;
       thr = thr_new;
-      if (near_len == 0 && far_len) thr = static_cast<uint64_t>(R[2]);  // jump: next refill opens [min, min + delta)
-      ++iter;
+      if (near_len == 0 && far_len) thr = static_cast<uint64_t>(R[3]);  // jump: the next window opens at the far minimum
       ++ph;
     }
-
+    const uint32_t reached = olen;
     tick(kProfCyclesRelax);
-    if (p.prof && tid == 0) atomicAdd(p.prof + kProfRounds, static_cast<unsigned long long>(iter));
-    // ---- B. the DAG: per vertex a successor mask (slots u->v with
-    // d(v) = d(u) + w) and a predecessor mask (d(u) = d(v) + w) in `flag`
-    // (free after A), successor counts, predecessor counts, reached count,
-    // max distance
-    if (tid == 0) {
-      s_reached = 0;
-      s_maxd = 0;
-    }
-    __syncthreads();
-    {
-      uint32_t reached = 0, maxd = 0;
-      for (uint32_t u = tid; u < n; u += T) {
-        const uint32_t du = __ldcg(dist + u);
-        if (du == kInfDist) continue;
-        ++reached;
-        maxd = max(maxd, du);
-        uint32_t b, e, sm = 0, pm = 0;
-        row_of(u, b, e);
-        for (uint32_t x = b; x < e; ++x) {
-          uint32_t v, wt;
-          load_slot<PACKED>(g, x, v, wt);
-          const uint32_t dv = __ldcg(dist + v);
-          if (dv == du + wt) {
-            sm |= 1u << (x - b);
-            atomicAdd(npred + v, 1u);
-          } else if (dv != kInfDist && dv + wt == du) {
-            pm |= 1u << (x - b);
-          }
-        }
-        nsucc[u] = __popc(sm);
-        flag[u] = sm | pm << 16;
-      }
-      reached = __reduce_add_sync(0xffffffffu, reached);
-      maxd = __reduce_max_sync(0xffffffffu, maxd);
-      if (lane == 0) {
-        atomicAdd(&s_reached, reached);
-        atomicMax(&s_maxd, maxd);
-      }
-    }
-    __syncthreads();
-    const uint32_t reached = s_reached, maxd = s_maxd;
-    tick(kProfCyclesThreshold);
-    if (static_cast<uint64_t>(maxd) >= w.n_stride) {
-      // distances beyond the counting-sort range: the team kernel runs this
-      // source instead (nothing has been accumulated yet)
-      if (tid == 0) w.abort_list[atomicAdd(w.abort_count, 1ULL)] = s_orig;
-      continue;
+    if (p.prof && tid == 0) {
+      atomicAdd(p.prof + kProfRounds, static_cast<unsigned long long>(ph));
+      atomicAdd(p.prof + kProfRefills, static_cast<unsigned long long>(windows));
     }
 
-    // ---- E1. counting sort of the distances and the sweep input
-    for (uint32_t i = tid; i <= maxd; i += T) hist[i] = 0;
-    __syncthreads();
-    constexpr int kH = 8;  // vertices per thread and step: their loads in flight together
-    for (uint32_t u0 = tid; u0 < n; u0 += T * kH) {
-      uint32_t du[kH];
-#pragma unroll
-      for (int j = 0; j < kH; ++j) du[j] = u0 + j * T < n ? __ldcg(dist + u0 + j * T) : kInfDist;
-#pragma unroll
-      for (int j = 0; j < kH; ++j)
-        if (du[j] != kInfDist) atomicAdd(hist + du[j], 1u);
-    }
-    if (tid == 0) s_carry = 0;
-    __syncthreads();
-    tick(kProfFarScanned);  // --prof: histogram
-    for (uint32_t base = 0; base <= maxd; base += T) {  // exclusive scan, T entries per step
-      const uint32_t i = base + tid;
-      const uint32_t x = i <= maxd ? hist[i] : 0u;
-      uint32_t incl = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= static_cast<uint32_t>(o)) incl += y;
-      }
-      if (lane == 31) s_warp[wid] = incl;
-      __syncthreads();
-      if (wid == 0) {
-        uint32_t ws = lane < T / 32 ? s_warp[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
-          if (lane >= static_cast<uint32_t>(o)) ws += y;
-        }
-        if (lane < T / 32) s_warp[lane] = ws;
-      }
-      __syncthreads();
-      const uint32_t before = s_carry + (wid ? s_warp[wid - 1] : 0u);
-      if (i <= maxd) hist[i] = before + incl - x;
-      __syncthreads();
-      if (tid == T - 1) s_carry = before + incl;
-      __syncthreads();
-    }
-    tick(kProfImprovements);  // --prof: scan
-    // scatter into distance order, writing each vertex's sweep input at its
-    // position: its slots u->v with d(v) > d(u) as (key d(u) + w + minw(v),
-    // d(v) + 1), zero pairs pad.  One vertex per thread and step, every
-    // load of a step in flight together (host: max degree <= kFlatMaxDeg).
-    uint32_t* const pos_of = w.q2 + off;  // sorted position per vertex (q2 is free after A)
-    for (uint32_t u0 = tid; u0 < n; u0 += T * kH) {
-      uint32_t du[kH], ps[kH];
-#pragma unroll
-      for (int j = 0; j < kH; ++j) du[j] = u0 + j * T < n ? __ldcg(dist + u0 + j * T) : kInfDist;
-#pragma unroll
-      for (int j = 0; j < kH; ++j) ps[j] = du[j] != kInfDist ? atomicAdd(hist + du[j], 1u) : 0u;
-#pragma unroll
-      for (int j = 0; j < kH; ++j)
-        if (du[j] != kInfDist) {
-          pos_of[u0 + j * T] = ps[j];
-          sorted_d[ps[j]] = du[j];
-        }
-    }
-    constexpr int kU = 1;
-    for (uint32_t u0 = tid; u0 < n; u0 += T * kU) {
-      uint32_t du[kU], pos[kU], rb[kU], re[kU];
+    // ---- B. sigma in distance order, a block of kBlkB positions at a time.
+    // Predecessors in earlier blocks are final (global psig); those inside
+    // the block are resolved by barrier rounds over the block's shared-memory
+    // copy (0 = not yet final: sigma >= 1).  The same pass writes per
+    // position the successor mask and positions, the sweep entries, and
+    // clears pcoef for pass C -- all coalesced.
+    for (uint32_t a = 0; a < reached; a += kBlkB) {
+      uint32_t v[kU], dv[kU], r[kU][KE], kk[kU][KE], sp[kU][KE], pend[kU];
+      uint2 nb[kU][KE];
+      double sg[kU];
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
-        const uint32_t u = u0 + j * T;
-        du[j] = u < n ? __ldcg(dist + u) : kInfDist;
-        rb[j] = re[j] = 0;
-        pos[j] = 0;
-        if (du[j] != kInfDist) {
-          row_of(u, rb[j], re[j]);
-          pos[j] = pos_of[u];
+        const uint32_t q = a + tid + j * T;
+        v[j] = q < reached ? __ldcg(order + q) : 0u;
+        dv[j] = q < reached ? __ldcg(ord_d + q) : kInfDist;
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        if (dv[j] != kInfDist) {
+          ell_row<KE>(w, v[j], r[j]);
+          ell_keys<KE>(w, v[j], kk[j]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < KE; ++x) r[j][x] = kk[j][x] = 0;
         }
       }
-      uint32_t v[kU][kFlatMaxDeg], wt[kU][kFlatMaxDeg], dv[kU][kFlatMaxDeg], mw[kU][kFlatMaxDeg];
 #pragma unroll
       for (int j = 0; j < kU; ++j)
 #pragma unroll
-        for (int x = 0; x < kFlatMaxDeg; ++x) {
-          v[j][x] = 0;
-          wt[j][x] = 0;
-          if (rb[j] + x < re[j]) load_slot<PACKED>(g, rb[j] + x, v[j][x], wt[j][x]);
-        }
-#pragma unroll
-      for (int j = 0; j < kU; ++j)
-#pragma unroll
-        for (int x = 0; x < kFlatMaxDeg; ++x) {
-          const bool ok = rb[j] + x < re[j];
-          dv[j][x] = ok ? __ldcg(dist + v[j][x]) : kInfDist;
-          mw[j][x] = ok ? __ldg(g.minw + v[j][x]) : 0u;
-        }
+        for (int x = 0; x < KE; ++x)
+          nb[j][x] = (r[j][x] & wmask) ? __ldcg(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
-        if (du[j] == kInfDist) continue;
-        uint2* const out = ivl + static_cast<uint64_t>(pos[j]) * kE;
-        int t = 0;
+        const uint32_t q = a + tid + j * T;
+        pend[j] = 0;
+        sg[j] = 0.0;
+        uint32_t pm = 0, sm = 0, e[KE];
 #pragma unroll
-        for (int x = 0; x < kFlatMaxDeg; ++x)
-          if (dv[j][x] != kInfDist && dv[j][x] > du[j]) out[t++] = make_uint2(du[j] + wt[j][x] + mw[j][x], dv[j][x] + 1);
-        for (; t < static_cast<int>(kE); ++t) out[t] = make_uint2(0, 0);
+        for (int x = 0; x < KE; ++x) {
+          const uint32_t wt = r[j][x] & wmask, d = nb[j][x].x;
+          e[x] = 0;
+          sp[j][x] = nb[j][x].y;
+          if (!wt || d == kInfDist) continue;  // padding (a reached vertex's neighbours are reached)
+          if (d + wt == dv[j]) pm |= 1u << x;
+          if (dv[j] + wt == d) sm |= 1u << x;
+          if (d > dv[j]) e[x] = kk[j][x] | (d - dv[j]) << 16;
+        }
+        if (q >= reached) continue;
+        __stcg(pcoef + q, 0.0);
+        __stcg(pinfo + q, sm | pm << 8);
+        uint4* const so = reinterpret_cast<uint4*>(psucc + static_cast<uint64_t>(q) * KE);
+        uint4* const eo = reinterpret_cast<uint4*>(ent + static_cast<uint64_t>(q) * KE);
+#pragma unroll
+        for (int x = 0; x < KE / 4; ++x) {
+          __stcg(so + x, make_uint4(sp[j][4 * x], sp[j][4 * x + 1], sp[j][4 * x + 2], sp[j][4 * x + 3]));
+          __stcg(eo + x, make_uint4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]));
+        }
+        if (q == 0) {
+          sg[j] = 1.0;  // the source (the only vertex at distance 0)
+        } else {
+#pragma unroll
+          for (int x = 0; x < KE; ++x)
+            if (pm >> x & 1u) {
+              if (sp[j][x] < a)
+                sg[j] += __ldcg(psig + sp[j][x]);
+              else
+                pend[j] |= 1u << x;
+            }
+        }
+        s_blk[q - a] = pend[j] ? 0.0 : sg[j];
       }
+      for (;;) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) any |= pend[j];
+        if (!__syncthreads_or(any)) break;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          if (!pend[j]) continue;
+#pragma unroll
+          for (int x = 0; x < KE; ++x)
+            if (pend[j] >> x & 1u) {
+              const double y = s_blk_v[sp[j][x] - a];
+              if (y != 0.0) {
+                sg[j] += y;
+                pend[j] &= ~(1u << x);
+              }
+            }
+          if (!pend[j]) s_blk_v[a + tid + j * T - a] = sg[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + tid + j * T;
+        if (q >= reached) continue;
+        note_sigma(p.overflow, sg[j]);
+        __stcg(psig + q, sg[j]);
+      }
+      __syncthreads();  // the block's sigma is visible to the next block's loads
     }
     __syncthreads();
-    for (uint32_t i = tid; i < w.buckets; i += T) bucket[i] = 0;
-    __syncthreads();
-    tick(kProfNearScanned);
-    // Warp 0 sweeps the Eq. 4 thresholds (E2) while the other warps run the
-    // sigma (C) and delta (D) dataflows; they synchronise on named barrier 1.
+    tick(kProfCyclesThreshold);
+
     if (wid == 0) {
-      // ---- E2. threshold sweep
+      // ---- C (warp 0). Eq. 4 threshold sweep over the sorted positions
       const uint32_t B = w.buckets, M = B - 1;
-      // bucket[k & M] = 1 + largest d(v) over inserted slots with key k; the
-      // key is live at threshold tau iff that d(v) >= tau
-      auto insert_slow = [&](uint32_t eb, uint32_t ee) {  // entries [eb, ee), 8 loads per lane in flight
-        for (uint32_t c0 = eb; c0 < ee; c0 += 256) {
-          uint2 kv[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t c = c0 + lane + 32 * j;
-            kv[j] = c < ee ? __ldcg(ivl + c) : make_uint2(0, 0);
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (kv[j].y) atomicMax(&bucket[kv[j].x & M], kv[j].y);
+      uint32_t* const bucket = hist;
+      uint32_t* const s_sd = smem + w.hist_words;
+      uint32_t* const s_en = s_sd + kFlatRing * kFlatChunk;
+      for (uint32_t i = lane; i < B; i += 32) bucket[i] = 0;
+      auto stage = [&](uint32_t c) {  // chunk c -> ring slot c % kFlatRing
+        if (c * kFlatChunk < reached) {
+          const uint32_t sl = c % kFlatRing;
+          for (uint32_t k = lane; k < kFlatChunk / 4; k += 32)
+            cp_async16(s_sd + sl * kFlatChunk + 4 * k, ord_d + c * kFlatChunk + 4 * k);
+          for (uint32_t k = lane; k < kFlatChunk * KE / 4; k += 32)
+            cp_async16(s_en + sl * kFlatChunk * KE + 4 * k,
+                       ent + static_cast<uint64_t>(c) * kFlatChunk * KE + 4 * k);
         }
+        cp_async_commit();
       };
-      // Lookahead registers, refilled at the end of each round for the next
-      // one: distances of sorted positions [sd_base, sd_base + 128) and sweep
-      // entries [iv_base, iv_base + 256) (positions iv_base / 8 ..).
-      uint32_t sd[4];
-      uint2 iv[8];
-      uint32_t sd_base = 0, iv_base = 0;
-      auto prefetch = [&](uint32_t q0) {
-        sd_base = q0;
-        iv_base = q0 * kE;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t q = q0 + lane + 32 * j;
-          sd[j] = q < reached ? __ldcg(sorted_d + q) : kInfDist;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t c = iv_base + lane + 32 * j;
-          iv[j] = c < reached * kE ? __ldcg(ivl + c) : make_uint2(0, 0);
-        }
-      };
-      uint32_t tau = 1, pos = 1, levels = 1;
-      insert_slow(0, kE);
+      uint32_t issued = 0, cur = 0;
+      for (; issued < static_cast<uint32_t>(kFlatRing); ++issued) stage(issued);
+      cp_async_wait<kFlatRing - 1>();
       __syncwarp();
-      prefetch(1);
+      auto ensure = [&](uint32_t q) {  // the chunk holding position q is resident (q only grows)
+        while (cur < q / kFlatChunk) {
+          __syncwarp();  // every lane is done with chunk cur's slot
+          ++cur;
+          stage(issued++);
+          cp_async_wait<kFlatRing - 1>();
+          __syncwarp();
+        }
+      };
+      constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
+      // insert the entries of positions [q, lim) with d < thr; returns how many qualified
+      auto take = [&](uint32_t q, uint32_t lim, uint32_t thr) -> uint32_t {
+        const uint32_t qq = q + lane;
+        const uint32_t d = qq < lim ? s_sd[qq % kRingPos] : kInfDist;
+        const bool in = d < thr;
+        if (in) {
+          const uint32_t* eq = s_en + (qq % kRingPos) * KE;
+#pragma unroll
+          for (int x = 0; x < KE; ++x) {
+            const uint32_t e = eq[x];
+            if (e) atomicMax(bucket + ((d + (e & 0xFFFFu)) & M), d + (e >> 16) + 1);
+          }
+        }
+        return __popc(__ballot_sync(0xffffffffu, in));  // a prefix: positions are sorted
+      };
+      __syncwarp();
+      take(0, 1, 1);  // level 0 = {s}
+      __syncwarp();
+      uint32_t tau = 1, pos = 1, levels = 1;
       for (;;) {
         uint32_t nxt = kInfDist;
         for (uint32_t base = tau + 1; base < tau + B; base += 32) {
@@ -448,100 +546,107 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         if (nxt == kInfDist) break;
         for (uint32_t k = tau + 1 + lane; k <= nxt; k += 32) bucket[k & M] = 0;
         __syncwarp();
-        // the new level: sorted positions [pos, end) with d < nxt (pos == sd_base)
-        uint32_t end = pos;
-        bool open = true;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const uint32_t m = __ballot_sync(0xffffffffu, sd[j] < nxt);
-          if (open) end += __popc(m);
-          open = open && m == 0xffffffffu;
+        // the new level: positions [pos, end) with d < nxt
+        uint32_t q = pos;
+        while (q < reached) {
+          ensure(q);
+          const uint32_t lim = min(min(q + 32, (q / kFlatChunk + 1) * kFlatChunk), reached);
+          const uint32_t got = take(q, lim, nxt);
+          q += got;
+          if (q < lim) break;
         }
-        while (open) {  // a level wider than the lookahead
-          const uint32_t q = end + lane;
-          const uint32_t m = __ballot_sync(0xffffffffu, q < reached && __ldcg(sorted_d + q) < nxt);
-          end += __popc(m);
-          open = m == 0xffffffffu;
-        }
-        // its sweep entries: from the lookahead, then the rest directly
-        const uint32_t eb = pos * kE, ee = end * kE;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t c = iv_base + lane + 32 * j;
-          if (c >= eb && c < ee && iv[j].y) atomicMax(&bucket[iv[j].x & M], iv[j].y);
-        }
-        if (ee > iv_base + 256) insert_slow(iv_base + 256, ee);
         __syncwarp();
-        pos = end;
+        pos = q;
         tau = nxt;
         ++levels;
-        prefetch(pos);
       }
+      cp_async_wait<0>();
       if (lane == 0 && p.depth) p.depth[s_orig] = levels;
     } else {
-      constexpr uint32_t TG = T - 32;  // dataflow threads
+      // ---- C (warps 1..). delta in reverse distance order, a block of kBlkC
+      // positions at a time (named barrier 1): successors in later blocks
+      // are final (global pcoef), those inside the block resolve by barrier
+      // rounds over its shared-memory copy.  Node BC += delta (u != s), edge
+      // BC += c.
+      constexpr uint32_t TG = T - 32;
       const uint32_t gt = tid - 32;
-      auto gsync = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(TG) : "memory"); };
-      // ---- C. sigma, forward dataflow over the DAG
-      uint32_t* const qf = w.q0 + off;
-      for (uint32_t i = gt; i < reached; i += TG) qf[i] = kFlatEmpty;
-      gsync();
-      if (gt == 0) {
-        sigma[s] = 1.0;
-        s_head = 0;
-        s_tail = 1;
-        st_vol(qf, s);
-      }
-      gsync();
-      for (;;) {
-        const uint32_t i = atomicAdd(&s_head, 1u);
-        if (i >= reached) break;
-        uint32_t u;
-        while ((u = ld_acq(qf + i)) == kFlatEmpty) __nanosleep(32);
-        const double su = __ldcg(sigma + u);
-        const uint32_t b = __ldg(g.offsets + u);
-        for (uint32_t sm = __ldcg(flag + u) & 0xFFFFu; sm; sm &= sm - 1) {
-          uint32_t v, wt;
-          load_slot<PACKED>(g, b + __ffs(sm) - 1, v, wt);
-          atomicAdd(sigma + v, su);
-          if (dec_acq_rel(npred + v) == 1u) st_rel(qf + atomicAdd(&s_tail, 1u), v);
+      for (uint32_t b = reached; b > 0;) {
+        const uint32_t a = b > kBlkC ? b - kBlkC : 0u;
+        uint32_t u[kU], sm[kU], sp[kU][KE];
+        double su[kU], dsum[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t i = gt + j * TG;  // q = b - 1 - i, in [a, b) when i < b - a
+          const bool ok = i < b - a;
+          const uint32_t q = ok ? b - 1 - i : 0u;
+          u[j] = ok ? __ldcg(order + q) : 0u;
+          sm[j] = ok ? __ldcg(pinfo + q) & 0xFFu : 0u;
+          su[j] = ok ? __ldcg(psig + q) : 1.0;
+          const uint4* so = reinterpret_cast<const uint4*>(psucc + static_cast<uint64_t>(q) * KE);
+#pragma unroll
+          for (int x = 0; x < KE / 4; ++x) {
+            const uint4 t4 = sm[j] ? __ldcg(so + x) : make_uint4(0, 0, 0, 0);
+            sp[j][4 * x] = t4.x;
+            sp[j][4 * x + 1] = t4.y;
+            sp[j][4 * x + 2] = t4.z;
+            sp[j][4 * x + 3] = t4.w;
+          }
         }
-      }
-      gsync();
-      // ---- D. delta, reverse dataflow; node / edge BC
-      uint32_t* const qb = w.q1 + off;
-      for (uint32_t i = gt; i < reached; i += TG) qb[i] = kFlatEmpty;
-      if (gt == 0) {
-        s_head = 0;
-        s_tail = 0;
-      }
-      gsync();
-      for (uint32_t u = gt; u < n; u += TG)  // the DAG's sinks start the sweep
-        if (__ldcg(dist + u) != kInfDist && nsucc[u] == 0) st_vol(qb + atomicAdd(&s_tail, 1u), u);
-      gsync();
-      for (;;) {
-        const uint32_t i = atomicAdd(&s_head, 1u);
-        if (i >= reached) break;
-        uint32_t v;
-        while ((v = ld_acq(qb + i)) == kFlatEmpty) __nanosleep(32);
-        const double dvv = __ldcg(delta + v);
-        const double sv = __ldcg(sigma + v);
-        if (v != s) atomicAdd(p.node_bc + v, dvv);
-        const uint32_t b = __ldg(g.offsets + v);
-        for (uint32_t pm = __ldcg(flag + v) >> 16; pm; pm &= pm - 1) {
-          const uint32_t x = b + __ffs(pm) - 1;
-          uint32_t u, wt;
-          load_slot<PACKED>(g, x, u, wt);
-          // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
-          const double c = __ldcg(sigma + u) / sv * (1.0 + dvv);
-          atomicAdd(delta + u, c);
-          if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + x), c);
-          if (dec_acq_rel(nsucc + u) == 1u) st_rel(qb + atomicAdd(&s_tail, 1u), u);
+        uint32_t pend[kU];
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t i = gt + j * TG;
+          dsum[j] = 0.0;
+          pend[j] = 0;
+#pragma unroll
+          for (int x = 0; x < KE; ++x) {
+            if (!(sm[j] >> x & 1u)) continue;
+            if (sp[j][x] >= b) {
+              const double c = su[j] * __ldcg(pcoef + sp[j][x]);
+              dsum[j] += c;
+              if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
+            } else {
+              pend[j] |= 1u << x;
+            }
+          }
+          if (i < b - a) s_blk[b - 1 - i - a] = pend[j] ? 0.0 : (1.0 + dsum[j]) / su[j];
         }
+        for (;;) {
+          uint32_t any = 0;
+#pragma unroll
+          for (int j = 0; j < kU; ++j) any |= pend[j];
+          if (!bar_or(any, 1, TG)) break;
+#pragma unroll
+          for (int j = 0; j < kU; ++j) {
+            if (!pend[j]) continue;
+#pragma unroll
+            for (int x = 0; x < KE; ++x)
+              if (pend[j] >> x & 1u) {
+                const double y = s_blk_v[sp[j][x] - a];
+                if (y != 0.0) {
+                  const double c = su[j] * y;
+                  dsum[j] += c;
+                  if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
+                  pend[j] &= ~(1u << x);
+                }
+              }
+            if (!pend[j]) s_blk_v[b - 1 - (gt + j * TG) - a] = (1.0 + dsum[j]) / su[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          const uint32_t i = gt + j * TG;
+          if (i >= b - a) continue;
+          const uint32_t q = b - 1 - i;
+          __stcg(pcoef + q, (1.0 + dsum[j]) / su[j]);
+          if (q != 0 && dsum[j] != 0.0) atomicAdd(p.node_bc + u[j], dsum[j]);  // not the source
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(TG) : "memory");  // the block's coef is visible to the next block
+        b = a;
       }
     }
     __syncthreads();
-    tick(kProfRefills);
+    tick(kProfCyclesBackward);
   }
 }
 

@@ -127,11 +127,13 @@ struct wbc_gpu_graph {
   void* d_ws = nullptr;
   uint64_t ws_bytes = 0;
   wbc_dev::Workspace ws{};
-  // the team-kernel layout of the same allocation that the flat kernel's
-  // handed-back sources are re-run on
-  wbc_dev::Workspace ws_fb{};
-  int fb_slots = 0;
   bool last_flat = false;     // the last run used bc_flat_kernel
+  // ELL copy of the rows for bc_flat_kernel (flat graphs only): per vertex a
+  // record of flat_ke slots and flat_ke sweep keys (weight + minw(neighbour)),
+  // and the slots' canonical edge ids
+  int flat_ke = 0;
+  uint32_t* d_ell = nullptr;
+  uint32_t* d_ell_eid = nullptr;
   int fill = 0;               // 2-CTA fill clusters beside a C >= 4 team launch
   // launch decisions are cached until a tuning knob changes
   uint64_t tune_gen = 1, shape_gen = 0, ws_gen = 0;
@@ -141,10 +143,6 @@ struct wbc_gpu_graph {
   int tune_fill = 0;          // opt-in: measured slower (R-MAT-24 C=16: 31.3 vs 32.5 GTEPS)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  uint32_t* d_abort_list = nullptr;
-  uint64_t abort_cap = 0;
-  unsigned long long* d_abort_count = nullptr;
-  unsigned long long* d_counter2 = nullptr;
   unsigned long long* d_counter = nullptr;
   unsigned int* d_overflow = nullptr;
   unsigned long long* d_prof = nullptr;
@@ -180,7 +178,7 @@ struct wbc_gpu_graph {
     if (side) cudaStreamDestroy(side);
     for (void* p : {(void*)d_offsets, (void*)d_slots32, (void*)d_slots64, (void*)d_minw,
                     (void*)d_edge_id, (void*)d_perm, (void*)d_inv, d_ws, (void*)d_counter,
-                    (void*)d_abort_list, (void*)d_abort_count, (void*)d_counter2,
+                    (void*)d_ell, (void*)d_ell_eid,
                     (void*)d_overflow, (void*)d_prof, (void*)d_node_dev, (void*)d_node,
                     (void*)d_edge, (void*)d_depth, (void*)d_sources, (void*)d_ref_slots32,
                     (void*)d_ref_slots64, (void*)d_ref_edge_id, (void*)d_stage})
@@ -249,9 +247,21 @@ uint32_t flat_buckets(const wbc_gpu_graph* g) {
   return b;
 }
 
+// window width of bc_flat_kernel's near-far SSSP
+uint32_t flat_delta(const wbc_gpu_graph* g) {
+  const uint32_t d = g->tune_flat_delta ? g->tune_flat_delta : std::max<uint32_t>(1, g->max_weight);
+  return std::min<uint32_t>(d, wbc_dev::kFlatBuckets);
+}
+uint32_t flat_hist_words(const wbc_gpu_graph* g) {
+  return std::max<uint32_t>(flat_buckets(g), (flat_delta(g) + 31) / 32 * 32);
+}
+
 bool flat_eligible(const wbc_gpu_graph* g) {
-  return g->n > 0 && g->symmetric && g->max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg) &&
-         flat_buckets(g) <= static_cast<uint32_t>(wbc_dev::kFlatBuckets);
+  // the ELL copy exists (packed slots, degree <= 8, mirror-image rows: the
+  // pull passes read a DAG edge from either end), the sweep keys fit the
+  // shared-memory ring, and threshold keys stay below 2^32
+  return g->n > 0 && g->d_ell && flat_buckets(g) <= static_cast<uint32_t>(wbc_dev::kFlatBuckets) &&
+         (uint64_t{g->n} - 1) * g->max_weight + 2ULL * flat_buckets(g) < 0xFFFFFFFFULL;
 }
 
 LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
@@ -265,7 +275,7 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   if ((g->tune_flat > 0 || auto_flat) && flat_eligible(g)) {
     s.flat = true;
     s.threads = kFlatT;
-    s.dyn_smem = flat_buckets(g) * 4;
+    s.dyn_smem = wbc_dev::flat_dyn_smem(flat_hist_words(g), g->flat_ke);
     return s;
   }
   const uint64_t n = g->n;
@@ -348,12 +358,16 @@ uint64_t ws_dcap(const wbc_gpu_graph* g) {
   const uint64_t n = g->n;
   return round_up(n + n / 2 + 1024, 64);
 }
+// bc_flat_kernel's per-source arrays: n_stride rounded to the
+// sweep ring's chunk, so a chunk copy never leaves the slot
+uint64_t flat_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, wbc_dev::kFlatChunk); }
 uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
-  return ws_ns(g) * (4 + 8 + 8 + 4 + 4 + 4 + 16 + 4 + 4 + 8 * uint64_t{std::max<uint32_t>(1, g->max_degree)});
+  const uint64_t ke = static_cast<uint64_t>(std::max(4, g->flat_ke));
+  return flat_ns(g) * (8 + 4 + 4 + 4 + 16 + 8 + 8 + 4 + 8 * ke);
 }
 
 void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
-  const uint64_t ns = ws_ns(g);
+  const uint64_t ns = flat_ns(g), ke = static_cast<uint64_t>(std::max(4, g->flat_ke));
   auto carve = [&](uint64_t bytes) {
     char* q = p;
     p += bytes * slots;
@@ -361,22 +375,24 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   };
   wbc_dev::FlatWs& w = g->fw;
   w.n_stride = ns;
-  w.sigma = reinterpret_cast<double*>(carve(ns * 8));
-  w.delta = reinterpret_cast<double*>(carve(ns * 8));
-  w.ivl_stride = std::max<uint32_t>(1, g->max_degree);
-  w.ivl = reinterpret_cast<uint2*>(carve(ns * 8 * w.ivl_stride));
-  w.dist = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.npred = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.nsucc = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.flag = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.dp = reinterpret_cast<uint2*>(carve(ns * 8));
+  w.psig = reinterpret_cast<double*>(carve(ns * 8));
+  w.pcoef = reinterpret_cast<double*>(carve(ns * 8));
+  w.psucc = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
+  w.ent = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
+  w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.mem = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q0 = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q1 = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q2 = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q3 = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.hist = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.sorted_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.delta_w = g->tune_flat_delta ? g->tune_flat_delta : std::max<uint32_t>(1, g->max_weight);
+  w.pinfo = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.ell = g->d_ell;
+  w.ell_eid = g->d_ell_eid;
+  w.delta_w = flat_delta(g);
   w.buckets = flat_buckets(g);
+  w.hist_words = flat_hist_words(g);
 }
 
 uint64_t ws_per_slot(const wbc_gpu_graph* g, bool team, bool one_warp = false) {
@@ -445,19 +461,13 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   const uint64_t per_slot = shape.flat ? ws_flat_per_slot(g) : ws_per_slot(g, team, one_warp);
   int slots = 0;
   if (shape.flat) {
-    const void* f = reinterpret_cast<const void*>(g->packed ? wbc_dev::bc_flat_kernel<kFlatT, true>
-                                                             : wbc_dev::bc_flat_kernel<kFlatT, false>);
+    const void* f = reinterpret_cast<const void*>(g->flat_ke == 4 ? wbc_dev::bc_flat_kernel<kFlatT, 4>
+                                                                   : wbc_dev::bc_flat_kernel<kFlatT, 8>);
     WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shape.dyn_smem)));
     int per_sm = 0;
     WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kFlatT, shape.dyn_smem));
     if (per_sm < 1) return set_error(WBC_E_CUDA, "flat kernel does not fit on an SM");
     slots = per_sm * g->sm_count;
-    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(1, 32, g->packed)),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(wbc_dev::team_dyn_smem(32))));
-    WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(1, 32, g->packed, true)),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(wbc_dev::team_dyn_smem(32))));
   }
   if (team) {
     for (const bool prof : {false, true}) {
@@ -531,15 +541,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   char* base = static_cast<char*>(g->d_ws);
   g->last_flat = shape.flat;
   if (shape.flat) {
-    // sources the flat kernel hands back run on one-warp teams over the same allocation
-    const uint64_t fb_per = ws_per_slot(g, true, true);
-    if (g->ws_bytes < fb_per) {
-      rc = ensure_bytes(g, fb_per);
-      if (rc) return rc;
-    }
     carve_flat(g, static_cast<char*>(g->d_ws), slots);
-    g->fb_slots = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(slots, g->ws_bytes / fb_per)));
-    g->ws_fb = carve_cta_team(g, static_cast<char*>(g->d_ws), g->fb_slots, true, true);
     g->ws_slots = slots;
     g->ws_team = false;
   } else {
@@ -637,39 +639,8 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     rc = launch_strict(g, shape, slots, p, k, edge_bc, d_edge, strict_lanes, stream);
     if (rc) return rc;
   } else if (shape.flat) {
-    if (g->abort_cap < k) {
-      cudaFree(g->d_abort_list);
-      cudaError_t e2 = cudaSuccess;
-      g->d_abort_list = dev_alloc<uint32_t>(k, e2);
-      if (e2 != cudaSuccess) {
-        g->abort_cap = 0;
-        return set_error(WBC_E_NOMEM, "abort list allocation failed");
-      }
-      g->abort_cap = k;
-    }
-    if (!g->d_abort_count) {
-      cudaError_t e2 = cudaSuccess;
-      g->d_abort_count = dev_alloc<unsigned long long>(2, e2);
-      if (e2 == cudaSuccess) g->d_counter2 = dev_alloc<unsigned long long>(1, e2);
-      if (e2 != cudaSuccess) return set_error(WBC_E_NOMEM, "counter allocation failed");
-    }
-    wbc_dev::FlatWs fw = g->fw;
-    fw.abort_list = g->d_abort_list;
-    fw.abort_count = g->d_abort_count;
-    WBC_CUDA_TRY(cudaMemsetAsync(g->d_abort_count, 0, sizeof(unsigned long long), stream));
-    WBC_CUDA_TRY(cudaMemsetAsync(g->d_counter2, 0, sizeof(unsigned long long), stream));
-    const auto fk = g->packed ? wbc_dev::bc_flat_kernel<kFlatT, true> : wbc_dev::bc_flat_kernel<kFlatT, false>;
-    fk<<<slots, kFlatT, shape.dyn_smem, stream>>>(p, fw);
-    WBC_CUDA_TRY(cudaGetLastError());
-    // sources whose distances left the counting-sort range: one-warp teams
-    p.ws = g->ws_fb;
-    p.sources = g->d_abort_list;
-    p.src_base = 0;
-    p.k = k;
-    p.k_dev = g->d_abort_count;
-    p.counter = g->d_counter2;
-    p.hot = 0;
-    pick_team(1, 32, g->packed, g->profiling)<<<g->fb_slots, 32, wbc_dev::team_dyn_smem(32), stream>>>(p);
+    const auto fk = g->flat_ke == 4 ? wbc_dev::bc_flat_kernel<kFlatT, 4> : wbc_dev::bc_flat_kernel<kFlatT, 8>;
+    fk<<<slots, kFlatT, shape.dyn_smem, stream>>>(p, g->fw);
     WBC_CUDA_TRY(cudaGetLastError());
   } else if (shape.cluster > 0) {
     // whole distance arrays of the few in-flight teams get evict-last
@@ -720,7 +691,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";
-  if (!strict_lanes) g->stats[3] = shape.flat ? 3 : (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
+  if (!strict_lanes) g->stats[3] = (shape.cluster > 0 && !single_slot && g->fill > 0) ? 3 : 2;
   return WBC_OK;
 }
 
@@ -835,6 +806,10 @@ struct HostCsr {
   double hot_coverage_25k = 0;
   std::vector<uint32_t> perm, inv, noff, slot32, eid, minw, ref_slot32, ref_eid;
   std::vector<uint2> slot64, ref_slot64;
+  // ELL copy for bc_flat_kernel (flat graphs): per vertex 2 ke words, the
+  // ke packed slots then ke u16 sweep keys (two per word), zero padded
+  int ke = 0;
+  std::vector<uint32_t> ell, ell_eid;
 };
 
 int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t* adjacency,
@@ -971,6 +946,27 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
         h.symmetric = twins == same && u != v;
       }
   }
+  // ELL rows for the distance-first kernel: packed slots, weight 0 pads
+  uint64_t max_key = 0;
+  for (uint32_t i = 0; i < n; ++i)
+    if (h.minw[i] != wbc_dev::kInfDist) max_key = std::max<uint64_t>(max_key, uint64_t{h.minw[i]} + maxw);
+  if (h.symmetric && packed && n > 0 && slots > 0 && max_key < 65536) {
+    const int ke = h.max_degree <= 4 ? 4 : 8;
+    h.ke = ke;
+    h.ell.assign(uint64_t{n} * 2 * ke, 0);
+    if (edge_id) h.ell_eid.assign(uint64_t{n} * ke, 0);
+    const uint32_t wm = (wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1);
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+      for (uint64_t v = b; v < e; ++v)
+        for (uint32_t j = 0; j < h.noff[v + 1] - h.noff[v]; ++j) {
+          const uint32_t x = h.slot32[h.noff[v] + j];
+          uint32_t* const rec = h.ell.data() + v * 2 * ke;
+          rec[j] = x;
+          rec[ke + j / 2] |= ((x & wm) + h.minw[x >> wbits]) << (16 * (j & 1));
+          if (edge_id) h.ell_eid[v * ke + j] = h.eid[h.noff[v] + j];
+        }
+    });
+  }
   return WBC_OK;
 }
 
@@ -1035,6 +1031,11 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   }
   if (err == cudaSuccess && h.has_edge_id) g->d_edge_id = dev_alloc<uint32_t>(slots, err);
   if (err == cudaSuccess && h.has_edge_id) g->d_ref_edge_id = dev_alloc<uint32_t>(slots, err);
+  g->flat_ke = h.ke;
+  if (err == cudaSuccess && h.ke) {
+    g->d_ell = dev_alloc<uint32_t>(h.ell.size(), err);
+    if (err == cudaSuccess && h.has_edge_id) g->d_ell_eid = dev_alloc<uint32_t>(h.ell_eid.size(), err);
+  }
   if (err != cudaSuccess) {
     delete g;
     return set_error(WBC_E_NOMEM, std::string("graph upload: ") + cudaGetErrorString(err));
@@ -1060,6 +1061,11 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
       err = cudaMemcpy(g->d_edge_id, h.eid.data(), slots * 4, cudaMemcpyHostToDevice);
     if (err == cudaSuccess && h.has_edge_id)
       err = cudaMemcpy(g->d_ref_edge_id, h.ref_eid.data(), slots * 4, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess && h.ke) {
+      err = cudaMemcpy(g->d_ell, h.ell.data(), h.ell.size() * 4, cudaMemcpyHostToDevice);
+      if (err == cudaSuccess && h.has_edge_id)
+        err = cudaMemcpy(g->d_ell_eid, h.ell_eid.data(), h.ell_eid.size() * 4, cudaMemcpyHostToDevice);
+    }
   }
   if (err != cudaSuccess) {
     delete g;
@@ -1067,6 +1073,7 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   }
   g->graph_bytes = (uint64_t{n} + 1) * 4 + uint64_t{n} * 12 + 2 * slots * (packed ? 4 : 8) +
                    (h.has_edge_id ? 2 * slots * 4 : 0);
+  g->graph_bytes += h.ell.size() * 4 + h.ell_eid.size() * 4;
   *out = g;
   return WBC_OK;
 }
@@ -1167,11 +1174,8 @@ int wbc_gpu_last_run_info(wbc_gpu_graph* g, uint64_t* out, uint32_t cap) {
   WBC_CUDA_TRY(cudaSetDevice(g->device));
   WBC_CUDA_TRY(cudaDeviceSynchronize());  // the run's device-side counters are final
   unsigned int ov[2] = {0, 0};
-  unsigned long long fb = 0;
-  if (g->stats[3]) {
-    WBC_CUDA_TRY(cudaMemcpy(ov, g->d_overflow, sizeof ov, cudaMemcpyDeviceToHost));
-    if (g->last_flat && g->d_abort_count) WBC_CUDA_TRY(cudaMemcpy(&fb, g->d_abort_count, 8, cudaMemcpyDeviceToHost));
-  }
+  const unsigned long long fb = 0;  // bc_flat_kernel completes every source (no hand-back since round 2)
+  if (g->stats[3]) WBC_CUDA_TRY(cudaMemcpy(ov, g->d_overflow, sizeof ov, cudaMemcpyDeviceToHost));
   const uint64_t v[WBC_RUN_INFO_FIELDS] = {g->stats[0], g->stats[1], ov[0], g->stats[3], fb, ov[1] ? 1u : 0u};
   for (uint32_t i = 0; i < cap && i < WBC_RUN_INFO_FIELDS; ++i) out[i] = v[i];
   return WBC_OK;

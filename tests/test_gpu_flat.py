@@ -1,7 +1,9 @@
 """GPU parity of the distance-first kernel for flat graphs (bc_flat.cuh,
-set_param("flat", 1)): near-far SSSP, dataflow sigma / delta, and the Eq. 4
-depth recovered from the distances by the threshold sweep.  Same bars as
-test_gpu_parity.py: BC 1e-9 relative, depth_per_source exact."""
+set_param("flat", 1)): near-far SSSP with window-sorted output, sigma / delta
+pulled in distance order, and the Eq. 4 depth recovered from the distances by
+the threshold sweep.  Same bars as test_gpu_parity.py: BC 1e-9 relative,
+depth_per_source exact.  Every run asserts the flat kernel did the work
+(flat_fallback_sources == 0: no source is handed to another kernel)."""
 import numpy as np
 import pytest
 
@@ -39,6 +41,7 @@ def test_flat_matches_oracle(W, oracle, delta):
             src = None if g.n <= 64 else W.sample_sources(g.n, 48, 3)
             check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
             assert gg.last_kernel() == "bc_flat_kernel", name
+            assert gg.last_run_stats()["flat_fallback_sources"] == 0, name
         finally:
             gg.close()
 
@@ -54,14 +57,31 @@ def test_flat_halved_duplicates_and_all_sources(W, oracle):
         gg.close()
 
 
-def test_flat_hands_long_distances_to_the_team_kernel(W, oracle):
-    """Distances beyond the counting-sort range (n_stride) abort to one-warp
-    teams before anything is accumulated."""
-    g = F.path_graph(40, w=1000.0)
-    gg = flat_graph(W, g)
+def test_flat_long_distances(W, oracle):
+    """Distances far beyond n (the round-1 kernel's counting-sort range, which
+    handed such sources to one-warp teams): the window sort only needs the
+    window width."""
+    for g in (F.path_graph(40, w=1000.0), W.build_csr(W.assign_weights(W.gen_grid(40, 31), 1, 1000, 7))):
+        gg = flat_graph(W, g)
+        try:
+            check_graph(W, oracle, g, edge=True, gg=gg)
+            assert gg.last_kernel() == "bc_flat_kernel"
+            assert gg.last_run_stats()["flat_fallback_sources"] == 0
+        finally:
+            gg.close()
+
+
+def test_flat_auto_grid512_vs_eq4_oracle(W, oracle):
+    """A 512x512 grid with the BASELINE weights 1-1000 (n = 2^18: the flat
+    kernel is picked automatically): node / edge BC and depth_per_source
+    against the oracle's Eq. 4 process."""
+    g = W.build_csr(W.assign_weights(W.gen_grid(512, 512), 1, 1000, 1))
+    src = W.sample_sources(g.n, 6, 1)
+    gg = W.GpuGraph(g)
     try:
-        check_graph(W, oracle, g, edge=True, gg=gg)
+        check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
         assert gg.last_kernel() == "bc_flat_kernel"
+        assert gg.last_run_stats()["flat_fallback_sources"] == 0
     finally:
         gg.close()
 
