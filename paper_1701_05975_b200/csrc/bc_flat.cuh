@@ -59,6 +59,14 @@ constexpr int kFlatMaxDeg = 8;        // ELL row width: 4 or 8 slots
 constexpr int kFlatBuckets = 16384;   // shared-memory keys: maxw + max minw + 2 must fit
 constexpr int kFlatChunk = 256;       // sweep ring: positions per chunk
 constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in flight)
+#ifndef WBC_FLAT_RELAX_U
+#define WBC_FLAT_RELAX_U 2
+#endif
+#ifndef WBC_FLAT_PRECHECK
+#define WBC_FLAT_PRECHECK 1
+#endif
+constexpr int kRelaxU = WBC_FLAT_RELAX_U;            // near vertices per thread and step in A
+constexpr bool kRelaxPrecheck = WBC_FLAT_PRECHECK;   // gather before the atomicMin
 
 struct FlatWs {
   uint64_t n_stride;        // multiple of kFlatChunk
@@ -248,35 +256,54 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       if (near_len) {
         // relax every near vertex: its ELL slots, then the neighbours'
         // distances, then the atomics (each stage's loads in flight together)
-        for (uint32_t i = tid; i < near_len; i += T) {
-          const uint32_t v = nq[i];
-          const uint32_t dv = __ldcg(dist_of(dp, v));
-          uint32_t r[KE], u[KE], nd[KE], old[KE];
-          ell_row<KE>(w, v, r);
+        for (uint32_t i0 = tid; i0 < near_len; i0 += T * kRelaxU) {
+          uint32_t dv[kRelaxU], r[kRelaxU][KE], nd[kRelaxU][KE], old[kRelaxU][KE];
 #pragma unroll
-          for (int x = 0; x < KE; ++x) {
-            const uint32_t wt = r[x] & wmask;
-            u[x] = r[x] >> wbits;
-            nd[x] = wt ? dv + wt : kInfDist;
+          for (int j = 0; j < kRelaxU; ++j) {
+            const uint32_t i = i0 + j * T;
+            const uint32_t v = i < near_len ? nq[i] : kInfDist;
+            dv[j] = v != kInfDist ? __ldcg(dist_of(dp, v)) : kInfDist;
+            if (v != kInfDist)
+              ell_row<KE>(w, v, r[j]);
+            else
+#pragma unroll
+              for (int x = 0; x < KE; ++x) r[j][x] = 0;
           }
 #pragma unroll
-          for (int x = 0; x < KE; ++x)
-            if (nd[x] != kInfDist && nd[x] >= __ldcg(dist_of(dp, u[x]))) nd[x] = kInfDist;
+          for (int j = 0; j < kRelaxU; ++j)
 #pragma unroll
-          for (int x = 0; x < KE; ++x) old[x] = nd[x] != kInfDist ? atomicMin(dist_of(dp, u[x]), nd[x]) : 0u;
-#pragma unroll
-          for (int x = 0; x < KE; ++x) {
-            if (nd[x] == kInfDist || nd[x] >= old[x]) continue;
-            if (nd[x] < thr32) {
-              // duplicates in the next near list are harmless (a re-relax
-              // reads the current distance); members are appended once, at
-              // the crossing below the window end
-              nn[atomicAdd(&R[0], 1u)] = u[x];
-              if (old[x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u[x];
-            } else if (old[x] == kInfDist) {
-              fq[far_len + atomicAdd(&R[1], 1u)] = u[x];
+            for (int x = 0; x < KE; ++x) {
+              const uint32_t wt = r[j][x] & wmask;
+              nd[j][x] = wt ? dv[j] + wt : kInfDist;
             }
+          if constexpr (kRelaxPrecheck) {
+#pragma unroll
+            for (int j = 0; j < kRelaxU; ++j)
+#pragma unroll
+              for (int x = 0; x < KE; ++x)
+                if (nd[j][x] != kInfDist && nd[j][x] >= __ldcg(dist_of(dp, r[j][x] >> wbits))) nd[j][x] = kInfDist;
           }
+#pragma unroll
+          for (int j = 0; j < kRelaxU; ++j)
+#pragma unroll
+            for (int x = 0; x < KE; ++x)
+              old[j][x] = nd[j][x] != kInfDist ? atomicMin(dist_of(dp, r[j][x] >> wbits), nd[j][x]) : 0u;
+#pragma unroll
+          for (int j = 0; j < kRelaxU; ++j)
+#pragma unroll
+            for (int x = 0; x < KE; ++x) {
+              if (nd[j][x] == kInfDist || nd[j][x] >= old[j][x]) continue;
+              const uint32_t u = r[j][x] >> wbits;
+              if (nd[j][x] < thr32) {
+                // duplicates in the next near list are harmless (a re-relax
+                // reads the current distance); members are appended once, at
+                // the crossing below the window end
+                nn[atomicAdd(&R[0], 1u)] = u;
+                if (old[j][x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u;
+              } else if (old[j][x] == kInfDist) {
+                fq[far_len + atomicAdd(&R[1], 1u)] = u;
+              }
+            }
         }
         __syncthreads();
         near_len = R[0];
@@ -482,7 +509,16 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     tick(kProfCyclesThreshold);
 
     if (wid == 0) {
-      // ---- C (warp 0). Eq. 4 threshold sweep over the sorted positions
+      // ---- C (warp 0). Eq. 4 threshold sweep over the sorted positions.
+      // bucket[k & M] = 1 + the largest d(v) over inserted slots u->v with
+      // key k; k is live at threshold tau iff that d(v) >= tau.  A slot's
+      // stale value (key k - B) is always below tau + 1 (its d(v) < k - B <
+      // tau), so slots are never cleared within a source.  Per level the
+      // smem scan for the next threshold and the level's position data
+      // (cp.async ring) are loaded together; the keys the level itself
+      // inserts enter the next threshold through a warp min in registers,
+      // so the scan never waits for its own atomics.
+      const unsigned long long t_sweep = clock64();
       const uint32_t B = w.buckets, M = B - 1;
       uint32_t* const bucket = hist;
       uint32_t* const s_sd = smem + w.hist_words;
@@ -499,69 +535,92 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         }
         cp_async_commit();
       };
+      // chunks [cur, cur + kFlatRing) are issued; cur and cur + 1 are complete
       uint32_t issued = 0, cur = 0;
       for (; issued < static_cast<uint32_t>(kFlatRing); ++issued) stage(issued);
-      cp_async_wait<kFlatRing - 1>();
+      cp_async_wait<kFlatRing - 2>();
       __syncwarp();
-      auto ensure = [&](uint32_t q) {  // the chunk holding position q is resident (q only grows)
+      auto advance_to = [&](uint32_t q) {  // position q (only grows) moves the window
         while (cur < q / kFlatChunk) {
           __syncwarp();  // every lane is done with chunk cur's slot
           ++cur;
           stage(issued++);
-          cp_async_wait<kFlatRing - 1>();
+          cp_async_wait<kFlatRing - 2>();
           __syncwarp();
         }
       };
       constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
-      // insert the entries of positions [q, lim) with d < thr; returns how many qualified
-      auto take = [&](uint32_t q, uint32_t lim, uint32_t thr) -> uint32_t {
-        const uint32_t qq = q + lane;
-        const uint32_t d = qq < lim ? s_sd[qq % kRingPos] : kInfDist;
-        const bool in = d < thr;
-        if (in) {
-          const uint32_t* eq = s_en + (qq % kRingPos) * KE;
-#pragma unroll
-          for (int x = 0; x < KE; ++x) {
-            const uint32_t e = eq[x];
-            if (e) atomicMax(bucket + ((d + (e & 0xFFFFu)) & M), d + (e >> 16) + 1);
-          }
-        }
-        return __popc(__ballot_sync(0xffffffffu, in));  // a prefix: positions are sorted
-      };
+      static_assert(kFlatChunk >= 64, "a 64-position block spans at most two chunks");
       __syncwarp();
-      take(0, 1, 1);  // level 0 = {s}
+      // level 0 = {s}: insert its entries (d(s) = 0)
+      uint32_t newmin = kInfDist;  // smallest key inserted by the last level, live at its threshold
+      if (lane < KE) {
+        const uint32_t e = s_en[lane];
+        if (e) {
+          atomicMax(bucket + ((e & 0xFFFFu) & M), (e >> 16) + 1);
+          newmin = e & 0xFFFFu;  // d(v) = e >> 16 >= 1 = tau: live
+        }
+      }
+      newmin = __reduce_min_sync(0xffffffffu, newmin);
       __syncwarp();
       uint32_t tau = 1, pos = 1, levels = 1;
       for (;;) {
-        uint32_t nxt = kInfDist;
-        for (uint32_t base = tau + 1; base < tau + B; base += 32) {
+        // the next threshold: the first live key > tau in the ring, or newmin
+        uint32_t nxt = newmin;
+        for (uint32_t base = tau + 1; base < tau + B && base <= nxt; base += 32) {
           const uint32_t k = base + lane;
           const bool live = k < tau + B && bucket[k & M] >= tau + 1;
           const uint32_t m = __ballot_sync(0xffffffffu, live);
           if (m) {
-            nxt = base + __ffs(m) - 1;
+            nxt = min(nxt, base + __ffs(m) - 1);
             break;
           }
         }
         if (nxt == kInfDist) break;
-        for (uint32_t k = tau + 1 + lane; k <= nxt; k += 32) bucket[k & M] = 0;
-        __syncwarp();
-        // the new level: positions [pos, end) with d < nxt
-        uint32_t q = pos;
+        // the new level: positions [pos, end) with d < nxt, 64 per block
+        uint32_t q = pos, lmin = kInfDist;
         while (q < reached) {
-          ensure(q);
-          const uint32_t lim = min(min(q + 32, (q / kFlatChunk + 1) * kFlatChunk), reached);
-          const uint32_t got = take(q, lim, nxt);
+          advance_to(q);
+          uint32_t d[2], e[2][KE];
+          bool in[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t qq = q + 32 * h + lane;
+            in[h] = qq < reached;
+            d[h] = in[h] ? s_sd[qq % kRingPos] : kInfDist;
+            const uint32_t* eq = s_en + (qq % kRingPos) * KE;
+#pragma unroll
+            for (int x = 0; x < KE; ++x) e[h][x] = in[h] ? eq[x] : 0u;
+          }
+          uint32_t got = 0;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            in[h] = in[h] && d[h] < nxt;
+            got += __popc(__ballot_sync(0xffffffffu, in[h]));  // a prefix: positions are sorted
+            if (!in[h]) continue;
+#pragma unroll
+            for (int x = 0; x < KE; ++x) {
+              const uint32_t ex = e[h][x];
+              const uint32_t dvp1 = d[h] + (ex >> 16) + 1;  // d(v) + 1
+              if (ex && dvp1 > nxt) {  // dead entries (v already settled) never matter again
+                const uint32_t key = d[h] + (ex & 0xFFFFu);
+                atomicMax(bucket + (key & M), dvp1);
+                lmin = min(lmin, key);
+              }
+            }
+          }
           q += got;
-          if (q < lim) break;
+          if (got < 64) break;
         }
-        __syncwarp();
+        newmin = __reduce_min_sync(0xffffffffu, lmin);
+        __syncwarp();  // this level's inserts are visible to the scans after the next one
         pos = q;
         tau = nxt;
         ++levels;
       }
       cp_async_wait<0>();
       if (lane == 0 && p.depth) p.depth[s_orig] = levels;
+      if (p.prof && lane == 0) atomicAdd(p.prof + kProfCyclesSettle, clock64() - t_sweep);  // the sweep alone
     } else {
       // ---- C (warps 1..). delta in reverse distance order, a block of kBlkC
       // positions at a time (named barrier 1): successors in later blocks
@@ -570,6 +629,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       // BC += c.
       constexpr uint32_t TG = T - 32;
       const uint32_t gt = tid - 32;
+      const unsigned long long t_delta = clock64();
       for (uint32_t b = reached; b > 0;) {
         const uint32_t a = b > kBlkC ? b - kBlkC : 0u;
         uint32_t u[kU], sm[kU], sp[kU][KE];
@@ -644,6 +704,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         asm volatile("bar.sync 1, %0;" ::"r"(TG) : "memory");  // the block's coef is visible to the next block
         b = a;
       }
+      if (p.prof && gt == 0) atomicAdd(p.prof + kProfNearScanned, clock64() - t_delta);  // the delta group alone
     }
     __syncthreads();
     tick(kProfCyclesBackward);
