@@ -72,7 +72,7 @@ struct FlatWs {
   uint64_t n_stride;        // multiple of kFlatChunk
   uint2* dp;                // by vertex: (distance, sorted position)
   uint32_t* order;          // by position: vertex in distance order
-  uint32_t* ord_d;          // by position: its distance
+  uint32_t* ord_d;          // by position: its distance (two buffers: the sweeper reads the last source's)
   uint32_t* mem;            // the open window's members (unsorted)
   uint32_t* q0;             // near / next near / far / next far queues
   uint32_t* q1;
@@ -83,12 +83,13 @@ struct FlatWs {
   uint32_t* pinfo;          // by position: successor mask | predecessor mask << 8
   uint32_t* psucc;          // by position: KE neighbour positions (successor slots only)
   uint32_t* ent;            // by position: KE sweep entries (w + minw(v)) | (d(v) - d(u)) << 16, 0 = none
+                            // (two buffers, like ord_d)
   const uint32_t* ell;      // n x 2KE words: KE slots (neighbour << wbits | weight, weight 0 = empty),
                             // KE u16 keys weight + minw(neighbour), padding to a 32-byte multiple
   const uint32_t* ell_eid;  // n x KE canonical edge ids (edge BC)
   uint32_t delta_w;         // window width (<= kFlatBuckets)
   uint32_t buckets;         // power of two >= maxw + max minw + 2
-  uint32_t hist_words;      // shared-memory words before the sweep ring: max(buckets, delta_w)
+  uint32_t delta_words;     // shared-memory words of the window-sort histogram (>= delta_w)
 };
 
 __device__ __forceinline__ double ld_relaxed_f64(const double* a) {
@@ -129,9 +130,10 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Dynamic shared memory of bc_flat_kernel<T, KE>.
-inline size_t flat_dyn_smem(uint32_t hist_words, int ke) {
-  return (static_cast<size_t>(hist_words) + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke)) * 4;
+// Dynamic shared memory of bc_flat_kernel<T, KE>: the workers' window-sort
+// histogram, then the sweeper's bucket ring and its cp.async ring.
+inline size_t flat_dyn_smem(uint32_t delta_words, uint32_t buckets, int ke) {
+  return (static_cast<size_t>(delta_words) + buckets + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke)) * 4;
 }
 
 // ELL record of v: 2 KE words (slots, then keys two per word)
@@ -172,357 +174,81 @@ __device__ __forceinline__ void ell_keys(const FlatWs& w, uint32_t v, uint32_t (
 }
 __device__ __forceinline__ uint32_t* dist_of(uint2* dp, uint32_t v) { return reinterpret_cast<uint32_t*>(dp + v); }
 
+// Named barriers of bc_flat_kernel (0 is __syncthreads, unused in the loop):
+// 1 = the worker group (warps 1..), 2 / 3 = buffer 0 / 1 ready for the
+// sweeper, 4 / 5 = buffer 0 / 1 released by the sweeper.
+template <int ID>
+__device__ __forceinline__ void nbar_sync(int count) {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+template <int ID>
+__device__ __forceinline__ void nbar_arrive(int count) {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(count) : "memory");
+}
+// buffer b's ready (2 + b) / released (4 + b) barriers
+template <int BASE>
+__device__ __forceinline__ void buf_sync(uint32_t b, int count) {
+  if (b) nbar_sync<BASE + 1>(count); else nbar_sync<BASE>(count);
+}
+template <int BASE>
+__device__ __forceinline__ void buf_arrive(uint32_t b, int count) {
+  if (b) nbar_arrive<BASE + 1>(count); else nbar_arrive<BASE>(count);
+}
+
 template <int T, int KE>
 __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p, const FlatWs w) {
   static_assert(KE == 4 || KE == 8, "ELL row width");
-  // p.prof: per-phase SM cycles of thread 0 (init -> kProfCyclesInit, A ->
-  // kProfCyclesRelax, B -> kProfCyclesThreshold, C -> kProfCyclesBackward),
-  // A's barrier phases -> kProfRounds, windows -> kProfRefills
-  unsigned long long t_last = 0;
-  auto tick = [&](int slot) {
-    if (p.prof && threadIdx.x == 0) {
-      const unsigned long long t = clock64();
-      if (slot >= 0) atomicAdd(p.prof + slot, t - t_last);
-      t_last = t;
-    }
-  };
+  constexpr uint32_t TG = T - 32;           // worker threads (warps 1..)
+  constexpr int kU = 2;                     // positions per thread in a pull block
+  constexpr uint32_t kBlk = TG * kU;        // pull block (passes B and C)
   __shared__ unsigned long long s_src;
-  __shared__ uint32_t s_ring[3][4];  // per-phase counters: [near, far, members, far min]
+  __shared__ uint32_t s_ring[3][4];          // per-phase counters: [near, far, members, far min]
   __shared__ uint32_t s_warp[T / 32];
-  constexpr int kU = 2;                  // positions per thread in a pull block
-  constexpr uint32_t kBlkB = T * kU;     // pass B block (all threads)
-  constexpr uint32_t kBlkC = (T - 32) * kU;  // pass C block (warps 1..)
-  __shared__ double s_blk[kBlkB];        // the block's sigma (B) / coef (C); 0 = not final
+  __shared__ double s_blk[kBlk];             // the block's sigma (B) / coef (C); 0 = not final
+  __shared__ uint32_t s_sw[2][3];            // per sweep buffer: reached, source, exit
   volatile double* const s_blk_v = s_blk;
-  extern __shared__ uint32_t smem[];  // [hist_words] hist / buckets, then the sweep ring
+  extern __shared__ uint32_t smem[];         // hist | buckets | sweep ring
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31, wid = tid >> 5;
   const uint64_t off = static_cast<uint64_t>(blockIdx.x) * w.n_stride;
   uint2* const dp = w.dp + off;
   uint32_t* const order = w.order + off;
-  uint32_t* const ord_d = w.ord_d + off;
   uint32_t* const mem = w.mem + off;
   double* const psig = w.psig + off;
   double* const pcoef = w.pcoef + off;
   uint32_t* const pinfo = w.pinfo + off;
   uint32_t* const psucc = w.psucc + off * KE;
-  uint32_t* const ent = w.ent + off * KE;
   uint32_t* const hist = smem;
+  uint32_t* const bucket = smem + w.delta_words;
   const uint32_t wbits = g.wbits, wmask = g.wmask;
+  // the sweep inputs are double-buffered: buffer b of this slot
+  auto ord_d_of = [&](uint32_t b) { return w.ord_d + (2 * off + b * w.n_stride); };
+  auto ent_of = [&](uint32_t b) { return w.ent + (2 * off + b * w.n_stride) * KE; };
 
-  for (;;) {
-    if (tid == 0) s_src = atomicAdd(p.counter, 1ULL);
-    __syncthreads();
-    const unsigned long long idx = s_src;
-    if (idx >= p.k) break;
-    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(p.src_base + idx);
-    const uint32_t s = __ldg(p.inv + s_orig);
-    tick(-1);
-
-    // ---- init: every word (infinite distance, position 0)
-    {
-      uint4* const d4 = reinterpret_cast<uint4*>(dp);
-      const uint32_t n2 = static_cast<uint32_t>(w.n_stride / 2);
-      for (uint32_t i = tid; i < n2; i += T) __stcg(d4 + i, make_uint4(kInfDist, 0u, kInfDist, 0u));
-    }
-    if (tid < 12) (&s_ring[0][0])[tid] = tid % 4 == 3 ? kInfDist : 0u;
-    __syncthreads();
-    if (tid == 0) {
-      *dist_of(dp, s) = 0;
-      w.q0[off] = s;
-      mem[0] = s;
-    }
-    __syncthreads();
-    tick(kProfCyclesInit);
-
-    // ---- A. near-far SSSP; windows sorted into `order` as they close
-    uint32_t* nq = w.q0 + off;
-    uint32_t* nn = w.q1 + off;
-    uint32_t* fq = w.q2 + off;
-    uint32_t* fq2 = w.q3 + off;
-    uint32_t near_len = 1, far_len = 0, mem_len = 1, olen = 0, ph = 0, windows = 0;
-    uint64_t lo = 0, thr = w.delta_w;
-    for (;;) {
-      uint32_t* R = s_ring[ph % 3];
-      if (tid == 0) {
-        uint32_t* Z = s_ring[(ph + 1) % 3];
-        Z[0] = 0;
-        Z[1] = 0;
-        Z[2] = 0;
-        Z[3] = kInfDist;
-      }
-      const uint32_t thr32 = thr >= kInfDist ? kInfDist : static_cast<uint32_t>(thr);
-      if (near_len) {
-        // relax every near vertex: its ELL slots, then the neighbours'
-        // distances, then the atomics (each stage's loads in flight together)
-        for (uint32_t i0 = tid; i0 < near_len; i0 += T * kRelaxU) {
-          uint32_t dv[kRelaxU], r[kRelaxU][KE], nd[kRelaxU][KE], old[kRelaxU][KE];
-#pragma unroll
-          for (int j = 0; j < kRelaxU; ++j) {
-            const uint32_t i = i0 + j * T;
-            const uint32_t v = i < near_len ? nq[i] : kInfDist;
-            dv[j] = v != kInfDist ? __ldcg(dist_of(dp, v)) : kInfDist;
-            if (v != kInfDist)
-              ell_row<KE>(w, v, r[j]);
-            else
-#pragma unroll
-              for (int x = 0; x < KE; ++x) r[j][x] = 0;
-          }
-#pragma unroll
-          for (int j = 0; j < kRelaxU; ++j)
-#pragma unroll
-            for (int x = 0; x < KE; ++x) {
-              const uint32_t wt = r[j][x] & wmask;
-              nd[j][x] = wt ? dv[j] + wt : kInfDist;
-            }
-          if constexpr (kRelaxPrecheck) {
-#pragma unroll
-            for (int j = 0; j < kRelaxU; ++j)
-#pragma unroll
-              for (int x = 0; x < KE; ++x)
-                if (nd[j][x] != kInfDist && nd[j][x] >= __ldcg(dist_of(dp, r[j][x] >> wbits))) nd[j][x] = kInfDist;
-          }
-#pragma unroll
-          for (int j = 0; j < kRelaxU; ++j)
-#pragma unroll
-            for (int x = 0; x < KE; ++x)
-              old[j][x] = nd[j][x] != kInfDist ? atomicMin(dist_of(dp, r[j][x] >> wbits), nd[j][x]) : 0u;
-#pragma unroll
-          for (int j = 0; j < kRelaxU; ++j)
-#pragma unroll
-            for (int x = 0; x < KE; ++x) {
-              if (nd[j][x] == kInfDist || nd[j][x] >= old[j][x]) continue;
-              const uint32_t u = r[j][x] >> wbits;
-              if (nd[j][x] < thr32) {
-                // duplicates in the next near list are harmless (a re-relax
-                // reads the current distance); members are appended once, at
-                // the crossing below the window end
-                nn[atomicAdd(&R[0], 1u)] = u;
-                if (old[j][x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u;
-              } else if (old[j][x] == kInfDist) {
-                fq[far_len + atomicAdd(&R[1], 1u)] = u;
-              }
-            }
-        }
-        __syncthreads();
-        near_len = R[0];
-        far_len += R[1];
-        mem_len += R[2];
-        uint32_t* t = nq;
-        nq = nn;
-        nn = t;
-        ++ph;
-        continue;
-      }
-      // the window [lo, thr) is closed: its members are final.  Counting
-      // sort on d - lo (< delta_w) appends them to order / ord_d and records
-      // each one's position; its sigma flag is cleared for pass B.
-      if (mem_len) {
-        const uint32_t span = static_cast<uint32_t>(thr - lo < w.delta_w ? thr - lo : w.delta_w);
-        for (uint32_t i = tid; i < span; i += T) hist[i] = 0;
-        __syncthreads();
-        for (uint32_t i = tid; i < mem_len; i += T) atomicAdd(hist + (__ldcg(dist_of(dp, mem[i])) - lo), 1u);
-        __syncthreads();
-        // exclusive scan of hist[0, span): a contiguous chunk per thread
-        const uint32_t per = (span + T - 1) / T, b0 = min(span, tid * per), b1 = min(span, b0 + per);
-        uint32_t loc = 0;
-        for (uint32_t i = b0; i < b1; ++i) loc += hist[i];
-        uint32_t incl = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= static_cast<uint32_t>(o)) incl += y;
-        }
-        if (lane == 31) s_warp[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-          uint32_t ws = lane < T / 32 ? s_warp[lane] : 0u;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
-            if (lane >= static_cast<uint32_t>(o)) ws += y;
-          }
-          if (lane < T / 32) s_warp[lane] = ws;
-        }
-        __syncthreads();
-        uint32_t run = olen + (wid ? s_warp[wid - 1] : 0u) + incl - loc;
-        for (uint32_t i = b0; i < b1; ++i) {
-          const uint32_t c = hist[i];
-          hist[i] = run;
-          run += c;
-        }
-        __syncthreads();
-        for (uint32_t i = tid; i < mem_len; i += T) {
-          const uint32_t u = mem[i];
-          const uint32_t du = __ldcg(dist_of(dp, u));
-          const uint32_t q = atomicAdd(hist + (du - lo), 1u);
-          order[q] = u;
-          ord_d[q] = du;
-          dp[u].y = q;
-          __stcg(psig + q, 0.0);
-        }
-        olen += mem_len;
-        mem_len = 0;
-        ++windows;
-        __syncthreads();
-      }
-      if (far_len == 0) break;
-      // next window [thr, thr + delta): far entries inside it become near
-      // (and members); the rest are compacted into the other far buffer
-      const uint64_t thr_new = thr + w.delta_w;
-      const uint32_t tn32 = thr_new >= kInfDist ? kInfDist : static_cast<uint32_t>(thr_new);
-      for (uint32_t i = tid; i < far_len; i += T) {
-        const uint32_t u = fq[i];
-        const uint32_t du = __ldcg(dist_of(dp, u));
-        if (du < thr32) continue;  // joined an earlier window: sorted already
-        if (du < tn32) {
-          nq[atomicAdd(&R[0], 1u)] = u;
-          mem[atomicAdd(&R[2], 1u)] = u;
-        } else {
-          fq2[atomicAdd(&R[1], 1u)] = u;
-          atomicMin(&R[3], du);
-        }
-      }
-      __syncthreads();
-      near_len = R[0];
-      far_len = R[1];
-      mem_len = R[2];
-      {
-        uint32_t* t = fq;
-        fq = fq2;
-        fq2 = t;
-      }
-      lo = thr;
-      thr = thr_new;
-      if (near_len == 0 && far_len) thr = static_cast<uint64_t>(R[3]);  // jump: the next window opens at the far minimum
-      ++ph;
-    }
-    const uint32_t reached = olen;
-    tick(kProfCyclesRelax);
-    if (p.prof && tid == 0) {
-      atomicAdd(p.prof + kProfRounds, static_cast<unsigned long long>(ph));
-      atomicAdd(p.prof + kProfRefills, static_cast<unsigned long long>(windows));
-    }
-
-    // ---- B. sigma in distance order, a block of kBlkB positions at a time.
-    // Predecessors in earlier blocks are final (global psig); those inside
-    // the block are resolved by barrier rounds over the block's shared-memory
-    // copy (0 = not yet final: sigma >= 1).  The same pass writes per
-    // position the successor mask and positions, the sweep entries, and
-    // clears pcoef for pass C -- all coalesced.
-    for (uint32_t a = 0; a < reached; a += kBlkB) {
-      uint32_t v[kU], dv[kU], r[kU][KE], kk[kU][KE], sp[kU][KE], pend[kU];
-      uint2 nb[kU][KE];
-      double sg[kU];
-#pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        const uint32_t q = a + tid + j * T;
-        v[j] = q < reached ? __ldcg(order + q) : 0u;
-        dv[j] = q < reached ? __ldcg(ord_d + q) : kInfDist;
-      }
-#pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        if (dv[j] != kInfDist) {
-          ell_row<KE>(w, v[j], r[j]);
-          ell_keys<KE>(w, v[j], kk[j]);
-        } else {
-#pragma unroll
-          for (int x = 0; x < KE; ++x) r[j][x] = kk[j][x] = 0;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kU; ++j)
-#pragma unroll
-        for (int x = 0; x < KE; ++x)
-          nb[j][x] = (r[j][x] & wmask) ? __ldcg(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
-#pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        const uint32_t q = a + tid + j * T;
-        pend[j] = 0;
-        sg[j] = 0.0;
-        uint32_t pm = 0, sm = 0, e[KE];
-#pragma unroll
-        for (int x = 0; x < KE; ++x) {
-          const uint32_t wt = r[j][x] & wmask, d = nb[j][x].x;
-          e[x] = 0;
-          sp[j][x] = nb[j][x].y;
-          if (!wt || d == kInfDist) continue;  // padding (a reached vertex's neighbours are reached)
-          if (d + wt == dv[j]) pm |= 1u << x;
-          if (dv[j] + wt == d) sm |= 1u << x;
-          if (d > dv[j]) e[x] = kk[j][x] | (d - dv[j]) << 16;
-        }
-        if (q >= reached) continue;
-        __stcg(pcoef + q, 0.0);
-        __stcg(pinfo + q, sm | pm << 8);
-        uint4* const so = reinterpret_cast<uint4*>(psucc + static_cast<uint64_t>(q) * KE);
-        uint4* const eo = reinterpret_cast<uint4*>(ent + static_cast<uint64_t>(q) * KE);
-#pragma unroll
-        for (int x = 0; x < KE / 4; ++x) {
-          __stcg(so + x, make_uint4(sp[j][4 * x], sp[j][4 * x + 1], sp[j][4 * x + 2], sp[j][4 * x + 3]));
-          __stcg(eo + x, make_uint4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]));
-        }
-        if (q == 0) {
-          sg[j] = 1.0;  // the source (the only vertex at distance 0)
-        } else {
-#pragma unroll
-          for (int x = 0; x < KE; ++x)
-            if (pm >> x & 1u) {
-              if (sp[j][x] < a)
-                sg[j] += __ldcg(psig + sp[j][x]);
-              else
-                pend[j] |= 1u << x;
-            }
-        }
-        s_blk[q - a] = pend[j] ? 0.0 : sg[j];
-      }
-      for (;;) {
-        uint32_t any = 0;
-#pragma unroll
-        for (int j = 0; j < kU; ++j) any |= pend[j];
-        if (!__syncthreads_or(any)) break;
-#pragma unroll
-        for (int j = 0; j < kU; ++j) {
-          if (!pend[j]) continue;
-#pragma unroll
-          for (int x = 0; x < KE; ++x)
-            if (pend[j] >> x & 1u) {
-              const double y = s_blk_v[sp[j][x] - a];
-              if (y != 0.0) {
-                sg[j] += y;
-                pend[j] &= ~(1u << x);
-              }
-            }
-          if (!pend[j]) s_blk_v[a + tid + j * T - a] = sg[j];
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        const uint32_t q = a + tid + j * T;
-        if (q >= reached) continue;
-        note_sigma(p.overflow, sg[j]);
-        __stcg(psig + q, sg[j]);
-      }
-      __syncthreads();  // the block's sigma is visible to the next block's loads
-    }
-    __syncthreads();
-    tick(kProfCyclesThreshold);
-
-    if (wid == 0) {
-      // ---- C (warp 0). Eq. 4 threshold sweep over the sorted positions.
-      // bucket[k & M] = 1 + the largest d(v) over inserted slots u->v with
-      // key k; k is live at threshold tau iff that d(v) >= tau.  A slot's
-      // stale value (key k - B) is always below tau + 1 (its d(v) < k - B <
-      // tau), so slots are never cleared within a source.  Per level the
-      // smem scan for the next threshold and the level's position data
-      // (cp.async ring) are loaded together; the keys the level itself
-      // inserts enter the next threshold through a warp min in registers,
-      // so the scan never waits for its own atomics.
+  if (wid == 0) {
+    // ===================== the sweeper (warp 0): Eq. 4 thresholds of the
+    // source the workers finished last, while they run the next one.
+    // bucket[k & M] = 1 + the largest d(v) over inserted slots u->v with
+    // key k; k is live at threshold tau iff that d(v) >= tau.  A slot's
+    // stale value (key k - B) is always below tau + 1 (its d(v) < k - B <
+    // tau), so slots are cleared only per source.  Per level the scan for the
+    // next threshold and the level's position data (cp.async ring) are loaded
+    // together; the keys the level itself inserts enter the next threshold
+    // through a warp min in registers.
+    const uint32_t B = w.buckets, M = B - 1;
+    uint32_t* const s_sd = bucket + B;
+    uint32_t* const s_en = s_sd + kFlatRing * kFlatChunk;
+    constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
+    static_assert(kFlatChunk >= 64, "a 64-position block spans at most two chunks");
+    for (uint32_t j = 0;; ++j) {
+      const uint32_t b = j & 1;
+      buf_sync<2>(b, T);
+      if (s_sw[b][2]) break;
       const unsigned long long t_sweep = clock64();
-      const uint32_t B = w.buckets, M = B - 1;
-      uint32_t* const bucket = hist;
-      uint32_t* const s_sd = smem + w.hist_words;
-      uint32_t* const s_en = s_sd + kFlatRing * kFlatChunk;
+      const uint32_t reached = s_sw[b][0], s_orig = s_sw[b][1];
+      const uint32_t* const ord_d = ord_d_of(b);
+      const uint32_t* const ent = ent_of(b);
       for (uint32_t i = lane; i < B; i += 32) bucket[i] = 0;
       auto stage = [&](uint32_t c) {  // chunk c -> ring slot c % kFlatRing
         if (c * kFlatChunk < reached) {
@@ -549,9 +275,6 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           __syncwarp();
         }
       };
-      constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
-      static_assert(kFlatChunk >= 64, "a 64-position block spans at most two chunks");
-      __syncwarp();
       // level 0 = {s}: insert its entries (d(s) = 0)
       uint32_t newmin = kInfDist;  // smallest key inserted by the last level, live at its threshold
       if (lane < KE) {
@@ -619,94 +342,447 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         ++levels;
       }
       cp_async_wait<0>();
+      __syncwarp();
       if (lane == 0 && p.depth) p.depth[s_orig] = levels;
-      if (p.prof && lane == 0) atomicAdd(p.prof + kProfCyclesSettle, clock64() - t_sweep);  // the sweep alone
-    } else {
-      // ---- C (warps 1..). delta in reverse distance order, a block of kBlkC
-      // positions at a time (named barrier 1): successors in later blocks
-      // are final (global pcoef), those inside the block resolve by barrier
-      // rounds over its shared-memory copy.  Node BC += delta (u != s), edge
-      // BC += c.
-      constexpr uint32_t TG = T - 32;
-      const uint32_t gt = tid - 32;
-      const unsigned long long t_delta = clock64();
-      for (uint32_t b = reached; b > 0;) {
-        const uint32_t a = b > kBlkC ? b - kBlkC : 0u;
-        uint32_t u[kU], sm[kU], sp[kU][KE];
-        double su[kU], dsum[kU];
+      if (p.prof && lane == 0) atomicAdd(p.prof + kProfCyclesSettle, clock64() - t_sweep);
+      buf_arrive<4>(b, T);  // buffer b is free again
+    }
+    return;
+  }
+
+  // ======================= the workers (warps 1..): SSSP, sigma, delta
+  const uint32_t gt = tid - 32, gw = wid - 1;  // worker thread / warp index
+  auto gsync = [&]() { nbar_sync<1>(TG); };
+  auto gsync_or = [&](uint32_t pred) { return bar_or(pred, 1, TG); };
+  // p.prof: per-phase SM cycles of worker 0 (init -> kProfCyclesInit, A ->
+  // kProfCyclesRelax, B -> kProfCyclesThreshold, C -> kProfCyclesBackward),
+  // A's barrier phases -> kProfRounds, windows -> kProfRefills; the sweeper
+  // adds its own cycles to kProfCyclesSettle
+  unsigned long long t_last = 0;
+  auto tick = [&](int slot) {
+    if (p.prof && gt == 0) {
+      const unsigned long long t = clock64();
+      if (slot >= 0) atomicAdd(p.prof + slot, t - t_last);
+      t_last = t;
+    }
+  };
+  uint32_t nsrc = 0;  // sources this CTA has run
+  for (;; ++nsrc) {
+    if (gt == 0) s_src = atomicAdd(p.counter, 1ULL);
+    gsync();
+    const unsigned long long idx = s_src;
+    const uint32_t b = nsrc & 1;
+    if (idx >= p.k) {
+      // release the sweeper: consume its last releases, signal the exit
+      if (nsrc >= 2) buf_sync<4>(b, T);
+      if (gt == 0) s_sw[b][2] = 1;
+      buf_arrive<2>(b, T);
+      if (nsrc >= 1) buf_sync<4>(b ^ 1, T);
+      break;
+    }
+    const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(p.src_base + idx);
+    const uint32_t s = __ldg(p.inv + s_orig);
+    tick(-1);
+    if (nsrc >= 2) buf_sync<4>(b, T);  // the sweeper is done with buffer b (source nsrc - 2)
+    uint32_t* const ord_d = ord_d_of(b);
+    uint32_t* const ent = ent_of(b);
+
+    // ---- init: every word (infinite distance, position 0)
+    {
+      uint4* const d4 = reinterpret_cast<uint4*>(dp);
+      const uint32_t n2 = static_cast<uint32_t>(w.n_stride / 2);
+      for (uint32_t i = gt; i < n2; i += TG) __stcg(d4 + i, make_uint4(kInfDist, 0u, kInfDist, 0u));
+    }
+    if (gt < 12) (&s_ring[0][0])[gt] = gt % 4 == 3 ? kInfDist : 0u;
+    gsync();
+    if (gt == 0) {
+      *dist_of(dp, s) = 0;
+      w.q0[off] = s;
+      mem[0] = s;
+    }
+    gsync();
+    tick(kProfCyclesInit);
+
+    // ---- A. near-far SSSP; windows sorted into `order` as they close
+    uint32_t* nq = w.q0 + off;
+    uint32_t* nn = w.q1 + off;
+    uint32_t* fq = w.q2 + off;
+    uint32_t* fq2 = w.q3 + off;
+    uint32_t near_len = 1, far_len = 0, mem_len = 1, olen = 0, ph = 0, windows = 0;
+    uint64_t lo = 0, thr = w.delta_w;
+    for (;;) {
+      uint32_t* R = s_ring[ph % 3];
+      if (gt == 0) {
+        uint32_t* Z = s_ring[(ph + 1) % 3];
+        Z[0] = 0;
+        Z[1] = 0;
+        Z[2] = 0;
+        Z[3] = kInfDist;
+      }
+      const uint32_t thr32 = thr >= kInfDist ? kInfDist : static_cast<uint32_t>(thr);
+      if (near_len) {
+        // relax every near vertex: its ELL slots, then the neighbours'
+        // distances, then the atomics (each stage's loads in flight together)
+        for (uint32_t i0 = gt; i0 < near_len; i0 += TG * kRelaxU) {
+          uint32_t dv[kRelaxU], r[kRelaxU][KE], nd[kRelaxU][KE], old[kRelaxU][KE];
 #pragma unroll
-        for (int j = 0; j < kU; ++j) {
-          const uint32_t i = gt + j * TG;  // q = b - 1 - i, in [a, b) when i < b - a
-          const bool ok = i < b - a;
-          const uint32_t q = ok ? b - 1 - i : 0u;
-          u[j] = ok ? __ldcg(order + q) : 0u;
-          sm[j] = ok ? __ldcg(pinfo + q) & 0xFFu : 0u;
-          su[j] = ok ? __ldcg(psig + q) : 1.0;
-          const uint4* so = reinterpret_cast<const uint4*>(psucc + static_cast<uint64_t>(q) * KE);
+          for (int j = 0; j < kRelaxU; ++j) {
+            const uint32_t i = i0 + j * TG;
+            const uint32_t v = i < near_len ? nq[i] : kInfDist;
+            dv[j] = v != kInfDist ? __ldcg(dist_of(dp, v)) : kInfDist;
+            if (v != kInfDist)
+              ell_row<KE>(w, v, r[j]);
+            else
 #pragma unroll
-          for (int x = 0; x < KE / 4; ++x) {
-            const uint4 t4 = sm[j] ? __ldcg(so + x) : make_uint4(0, 0, 0, 0);
-            sp[j][4 * x] = t4.x;
-            sp[j][4 * x + 1] = t4.y;
-            sp[j][4 * x + 2] = t4.z;
-            sp[j][4 * x + 3] = t4.w;
+              for (int x = 0; x < KE; ++x) r[j][x] = 0;
           }
-        }
-        uint32_t pend[kU];
 #pragma unroll
-        for (int j = 0; j < kU; ++j) {
-          const uint32_t i = gt + j * TG;
-          dsum[j] = 0.0;
-          pend[j] = 0;
+          for (int j = 0; j < kRelaxU; ++j)
 #pragma unroll
-          for (int x = 0; x < KE; ++x) {
-            if (!(sm[j] >> x & 1u)) continue;
-            if (sp[j][x] >= b) {
-              const double c = su[j] * __ldcg(pcoef + sp[j][x]);
-              dsum[j] += c;
-              if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
-            } else {
-              pend[j] |= 1u << x;
+            for (int x = 0; x < KE; ++x) {
+              const uint32_t wt = r[j][x] & wmask;
+              nd[j][x] = wt ? dv[j] + wt : kInfDist;
             }
+          if constexpr (kRelaxPrecheck) {
+#pragma unroll
+            for (int j = 0; j < kRelaxU; ++j)
+#pragma unroll
+              for (int x = 0; x < KE; ++x)
+                if (nd[j][x] != kInfDist && nd[j][x] >= __ldcg(dist_of(dp, r[j][x] >> wbits))) nd[j][x] = kInfDist;
           }
-          if (i < b - a) s_blk[b - 1 - i - a] = pend[j] ? 0.0 : (1.0 + dsum[j]) / su[j];
-        }
-        for (;;) {
-          uint32_t any = 0;
 #pragma unroll
-          for (int j = 0; j < kU; ++j) any |= pend[j];
-          if (!bar_or(any, 1, TG)) break;
-#pragma unroll
-          for (int j = 0; j < kU; ++j) {
-            if (!pend[j]) continue;
+          for (int j = 0; j < kRelaxU; ++j)
 #pragma unroll
             for (int x = 0; x < KE; ++x)
-              if (pend[j] >> x & 1u) {
-                const double y = s_blk_v[sp[j][x] - a];
-                if (y != 0.0) {
-                  const double c = su[j] * y;
-                  dsum[j] += c;
-                  if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
-                  pend[j] &= ~(1u << x);
-                }
+              old[j][x] = nd[j][x] != kInfDist ? atomicMin(dist_of(dp, r[j][x] >> wbits), nd[j][x]) : 0u;
+#pragma unroll
+          for (int j = 0; j < kRelaxU; ++j)
+#pragma unroll
+            for (int x = 0; x < KE; ++x) {
+              if (nd[j][x] == kInfDist || nd[j][x] >= old[j][x]) continue;
+              const uint32_t u = r[j][x] >> wbits;
+              if (nd[j][x] < thr32) {
+                // duplicates in the next near list are harmless (a re-relax
+                // reads the current distance); members are appended once, at
+                // the crossing below the window end
+                nn[atomicAdd(&R[0], 1u)] = u;
+                if (old[j][x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u;
+              } else if (old[j][x] == kInfDist) {
+                fq[far_len + atomicAdd(&R[1], 1u)] = u;
               }
-            if (!pend[j]) s_blk_v[b - 1 - (gt + j * TG) - a] = (1.0 + dsum[j]) / su[j];
+            }
+        }
+        gsync();
+        near_len = R[0];
+        far_len += R[1];
+        mem_len += R[2];
+        uint32_t* t = nq;
+        nq = nn;
+        nn = t;
+        ++ph;
+        continue;
+      }
+      // the window [lo, thr) is closed: its members are final.  Counting
+      // sort on d - lo (< delta_w) appends them to order / ord_d and records
+      // each one's position; its sigma flag is cleared for pass B.
+      if (mem_len) {
+        const uint32_t span = static_cast<uint32_t>(thr - lo < w.delta_w ? thr - lo : w.delta_w);
+        for (uint32_t i = gt; i < span; i += TG) hist[i] = 0;
+        gsync();
+        constexpr int kM = 4;  // members per thread and step, gathers in flight together
+        for (uint32_t i0 = gt; i0 < mem_len; i0 += TG * kM) {
+          uint32_t u[kM], du[kM];
+#pragma unroll
+          for (int j = 0; j < kM; ++j) u[j] = i0 + j * TG < mem_len ? mem[i0 + j * TG] : kInfDist;
+#pragma unroll
+          for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+#pragma unroll
+          for (int j = 0; j < kM; ++j)
+            if (u[j] != kInfDist) atomicAdd(hist + (du[j] - lo), 1u);
+        }
+        gsync();
+        // exclusive scan of hist[0, span): a contiguous chunk per thread
+        const uint32_t per = (span + TG - 1) / TG, b0 = min(span, gt * per), b1 = min(span, b0 + per);
+        uint32_t loc = 0;
+        for (uint32_t i = b0; i < b1; ++i) loc += hist[i];
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= static_cast<uint32_t>(o)) incl += y;
+        }
+        if (lane == 31) s_warp[gw] = incl;
+        gsync();
+        if (gw == 0) {
+          uint32_t ws = lane < TG / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= static_cast<uint32_t>(o)) ws += y;
+          }
+          if (lane < TG / 32) s_warp[lane] = ws;
+        }
+        gsync();
+        uint32_t run = olen + (gw ? s_warp[gw - 1] : 0u) + incl - loc;
+        for (uint32_t i = b0; i < b1; ++i) {
+          const uint32_t c = hist[i];
+          hist[i] = run;
+          run += c;
+        }
+        gsync();
+        for (uint32_t i0 = gt; i0 < mem_len; i0 += TG * kM) {
+          uint32_t u[kM], du[kM];
+#pragma unroll
+          for (int j = 0; j < kM; ++j) u[j] = i0 + j * TG < mem_len ? mem[i0 + j * TG] : kInfDist;
+#pragma unroll
+          for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+#pragma unroll
+          for (int j = 0; j < kM; ++j) {
+            if (u[j] == kInfDist) continue;
+            const uint32_t q = atomicAdd(hist + (du[j] - lo), 1u);
+            order[q] = u[j];
+            ord_d[q] = du[j];
+            dp[u[j]].y = q;
+            __stcg(psig + q, 0.0);
           }
         }
+        olen += mem_len;
+        mem_len = 0;
+        ++windows;
+        gsync();
+      }
+      if (far_len == 0) break;
+      // next window [thr, thr + delta): far entries inside it become near
+      // (and members); the rest are compacted into the other far buffer
+      const uint64_t thr_new = thr + w.delta_w;
+      const uint32_t tn32 = thr_new >= kInfDist ? kInfDist : static_cast<uint32_t>(thr_new);
+      constexpr int kF = 4;  // far entries per thread and step, gathers in flight together
+      for (uint32_t i0 = gt; i0 < far_len; i0 += TG * kF) {
+        uint32_t u[kF], du[kF];
+#pragma unroll
+        for (int j = 0; j < kF; ++j) u[j] = i0 + j * TG < far_len ? fq[i0 + j * TG] : kInfDist;
+#pragma unroll
+        for (int j = 0; j < kF; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+#pragma unroll
+        for (int j = 0; j < kF; ++j) {
+          if (u[j] == kInfDist || du[j] < thr32) continue;  // joined an earlier window: sorted already
+          if (du[j] < tn32) {
+            nq[atomicAdd(&R[0], 1u)] = u[j];
+            mem[atomicAdd(&R[2], 1u)] = u[j];
+          } else {
+            fq2[atomicAdd(&R[1], 1u)] = u[j];
+            atomicMin(&R[3], du[j]);
+          }
+        }
+      }
+      gsync();
+      near_len = R[0];
+      far_len = R[1];
+      mem_len = R[2];
+      {
+        uint32_t* t = fq;
+        fq = fq2;
+        fq2 = t;
+      }
+      lo = thr;
+      thr = thr_new;
+      if (near_len == 0 && far_len) thr = static_cast<uint64_t>(R[3]);  // jump: the next window opens at the far minimum
+      ++ph;
+    }
+    const uint32_t reached = olen;
+    tick(kProfCyclesRelax);
+    if (p.prof && gt == 0) {
+      atomicAdd(p.prof + kProfRounds, static_cast<unsigned long long>(ph));
+      atomicAdd(p.prof + kProfRefills, static_cast<unsigned long long>(windows));
+    }
+
+    // ---- B. sigma in distance order, a block of kBlk positions at a time.
+    // Predecessors in earlier blocks are final (global psig); those inside
+    // the block are resolved by barrier rounds over the block's shared-memory
+    // copy (0 = not yet final: sigma >= 1).  The same pass writes per
+    // position the successor mask and positions, the sweep entries, and
+    // clears pcoef for pass C -- all coalesced.
+    for (uint32_t a = 0; a < reached; a += kBlk) {
+      uint32_t v[kU], dv[kU], r[kU][KE], kk[kU][KE], sp[kU][KE], pend[kU];
+      uint2 nb[kU][KE];
+      double sg[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + gt + j * TG;
+        v[j] = q < reached ? __ldcg(order + q) : 0u;
+        dv[j] = q < reached ? __ldcg(ord_d + q) : kInfDist;
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        if (dv[j] != kInfDist) {
+          ell_row<KE>(w, v[j], r[j]);
+          ell_keys<KE>(w, v[j], kk[j]);
+        } else {
+#pragma unroll
+          for (int x = 0; x < KE; ++x) r[j][x] = kk[j][x] = 0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j)
+#pragma unroll
+        for (int x = 0; x < KE; ++x)
+          nb[j][x] = (r[j][x] & wmask) ? __ldcg(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + gt + j * TG;
+        pend[j] = 0;
+        sg[j] = 0.0;
+        uint32_t pm = 0, sm = 0, e[KE];
+#pragma unroll
+        for (int x = 0; x < KE; ++x) {
+          const uint32_t wt = r[j][x] & wmask, d = nb[j][x].x;
+          e[x] = 0;
+          sp[j][x] = nb[j][x].y;
+          if (!wt || d == kInfDist) continue;  // padding (a reached vertex's neighbours are reached)
+          if (d + wt == dv[j]) pm |= 1u << x;
+          if (dv[j] + wt == d) sm |= 1u << x;
+          if (d > dv[j]) e[x] = kk[j][x] | (d - dv[j]) << 16;
+        }
+        if (q >= reached) continue;
+        __stcg(pcoef + q, 0.0);
+        __stcg(pinfo + q, sm | pm << 8);
+        uint4* const so = reinterpret_cast<uint4*>(psucc + static_cast<uint64_t>(q) * KE);
+        uint4* const eo = reinterpret_cast<uint4*>(ent + static_cast<uint64_t>(q) * KE);
+#pragma unroll
+        for (int x = 0; x < KE / 4; ++x) {
+          __stcg(so + x, make_uint4(sp[j][4 * x], sp[j][4 * x + 1], sp[j][4 * x + 2], sp[j][4 * x + 3]));
+          __stcg(eo + x, make_uint4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]));
+        }
+        if (q == 0) {
+          sg[j] = 1.0;  // the source (the only vertex at distance 0)
+        } else {
+#pragma unroll
+          for (int x = 0; x < KE; ++x)
+            if (pm >> x & 1u) {
+              if (sp[j][x] < a)
+                sg[j] += __ldcg(psig + sp[j][x]);
+              else
+                pend[j] |= 1u << x;
+            }
+        }
+        s_blk[q - a] = pend[j] ? 0.0 : sg[j];
+      }
+      for (;;) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) any |= pend[j];
+        if (!gsync_or(any)) break;
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
-          const uint32_t i = gt + j * TG;
-          if (i >= b - a) continue;
-          const uint32_t q = b - 1 - i;
-          __stcg(pcoef + q, (1.0 + dsum[j]) / su[j]);
-          if (q != 0 && dsum[j] != 0.0) atomicAdd(p.node_bc + u[j], dsum[j]);  // not the source
+          if (!pend[j]) continue;
+#pragma unroll
+          for (int x = 0; x < KE; ++x)
+            if (pend[j] >> x & 1u) {
+              const double y = s_blk_v[sp[j][x] - a];
+              if (y != 0.0) {
+                sg[j] += y;
+                pend[j] &= ~(1u << x);
+              }
+            }
+          if (!pend[j]) s_blk_v[gt + j * TG] = sg[j];
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(TG) : "memory");  // the block's coef is visible to the next block
-        b = a;
       }
-      if (p.prof && gt == 0) atomicAdd(p.prof + kProfNearScanned, clock64() - t_delta);  // the delta group alone
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + gt + j * TG;
+        if (q >= reached) continue;
+        note_sigma(p.overflow, sg[j]);
+        __stcg(psig + q, sg[j]);
+      }
+      gsync();  // the block's sigma is visible to the next block's loads
     }
-    __syncthreads();
+    tick(kProfCyclesThreshold);
+    // hand the distances and entries to the sweeper (buffer b)
+    if (gt == 0) {
+      s_sw[b][0] = reached;
+      s_sw[b][1] = s_orig;
+      s_sw[b][2] = 0;
+    }
+    buf_arrive<2>(b, T);
+
+    // ---- C. delta in reverse distance order, a block of kBlk positions at a
+    // time: successors in later blocks are final (global pcoef), those inside
+    // the block resolve by barrier rounds over its shared-memory copy.  Node
+    // BC += delta (u != s), edge BC += c.
+    for (uint32_t bend = reached; bend > 0;) {
+      const uint32_t a = bend > kBlk ? bend - kBlk : 0u;
+      uint32_t u[kU], sm[kU], sp[kU][KE];
+      double su[kU], dsum[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t i = gt + j * TG;  // q = bend - 1 - i, in [a, bend) when i < bend - a
+        const bool ok = i < bend - a;
+        const uint32_t q = ok ? bend - 1 - i : 0u;
+        u[j] = ok ? __ldcg(order + q) : 0u;
+        sm[j] = ok ? __ldcg(pinfo + q) & 0xFFu : 0u;
+        su[j] = ok ? __ldcg(psig + q) : 1.0;
+        const uint4* so = reinterpret_cast<const uint4*>(psucc + static_cast<uint64_t>(q) * KE);
+#pragma unroll
+        for (int x = 0; x < KE / 4; ++x) {
+          const uint4 t4 = sm[j] ? __ldcg(so + x) : make_uint4(0, 0, 0, 0);
+          sp[j][4 * x] = t4.x;
+          sp[j][4 * x + 1] = t4.y;
+          sp[j][4 * x + 2] = t4.z;
+          sp[j][4 * x + 3] = t4.w;
+        }
+      }
+      uint32_t pend[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t i = gt + j * TG;
+        dsum[j] = 0.0;
+        pend[j] = 0;
+#pragma unroll
+        for (int x = 0; x < KE; ++x) {
+          if (!(sm[j] >> x & 1u)) continue;
+          if (sp[j][x] >= bend) {
+            const double c = su[j] * __ldcg(pcoef + sp[j][x]);
+            dsum[j] += c;
+            if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
+          } else {
+            pend[j] |= 1u << x;
+          }
+        }
+        if (i < bend - a) s_blk[bend - 1 - i - a] = pend[j] ? 0.0 : (1.0 + dsum[j]) / su[j];
+      }
+      for (;;) {
+        uint32_t any = 0;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) any |= pend[j];
+        if (!gsync_or(any)) break;
+#pragma unroll
+        for (int j = 0; j < kU; ++j) {
+          if (!pend[j]) continue;
+#pragma unroll
+          for (int x = 0; x < KE; ++x)
+            if (pend[j] >> x & 1u) {
+              const double y = s_blk_v[sp[j][x] - a];
+              if (y != 0.0) {
+                const double c = su[j] * y;
+                dsum[j] += c;
+                if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
+                pend[j] &= ~(1u << x);
+              }
+            }
+          if (!pend[j]) s_blk_v[bend - 1 - (gt + j * TG) - a] = (1.0 + dsum[j]) / su[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t i = gt + j * TG;
+        if (i >= bend - a) continue;
+        const uint32_t q = bend - 1 - i;
+        __stcg(pcoef + q, (1.0 + dsum[j]) / su[j]);
+        if (q != 0 && dsum[j] != 0.0) atomicAdd(p.node_bc + u[j], dsum[j]);  // not the source
+      }
+      gsync();  // the block's coef is visible to the next block
+      bend = a;
+    }
     tick(kProfCyclesBackward);
   }
 }

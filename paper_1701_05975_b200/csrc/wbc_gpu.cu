@@ -161,6 +161,7 @@ struct wbc_gpu_graph {
   bool tune_near = false;      // near_width set explicitly (else the launch shape may adjust it)
   int tune_flat = -1;          // -1 auto (flat, large graphs), 0 off, 1 wherever eligible
   uint32_t tune_flat_delta = 0;  // near-far window of bc_flat_kernel (0: max weight)
+  int tune_flat_threads = 0;     // bc_flat_kernel CTA size (0: kFlatT)
   uint32_t max_degree = 0, max_minw = 0;
   bool symmetric = false;
   wbc_dev::FlatWs fw{};
@@ -238,7 +239,15 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g);
 LaunchShape pick_shape(wbc_gpu_graph* g);
 
 // bc_flat_kernel: CTA size (two CTAs per SM: its phases are latency-bound)
-constexpr int kFlatT = 512;
+constexpr int kFlatT = 512;  // default; set_param("flat_threads", 256 | 512 | 1024)
+
+using FlatFn = void (*)(const wbc_dev::RunParams, const wbc_dev::FlatWs);
+FlatFn pick_flat(int threads, int ke) {
+  using namespace wbc_dev;
+  if (threads <= 256) return ke == 4 ? bc_flat_kernel<256, 4> : bc_flat_kernel<256, 8>;
+  if (threads <= 512) return ke == 4 ? bc_flat_kernel<512, 4> : bc_flat_kernel<512, 8>;
+  return ke == 4 ? bc_flat_kernel<1024, 4> : bc_flat_kernel<1024, 8>;
+}
 
 // bc_flat_kernel's bucket array: a power of two > max weight + max minw + 1.
 uint32_t flat_buckets(const wbc_gpu_graph* g) {
@@ -252,9 +261,7 @@ uint32_t flat_delta(const wbc_gpu_graph* g) {
   const uint32_t d = g->tune_flat_delta ? g->tune_flat_delta : std::max<uint32_t>(1, g->max_weight);
   return std::min<uint32_t>(d, wbc_dev::kFlatBuckets);
 }
-uint32_t flat_hist_words(const wbc_gpu_graph* g) {
-  return std::max<uint32_t>(flat_buckets(g), (flat_delta(g) + 31) / 32 * 32);
-}
+uint32_t flat_delta_words(const wbc_gpu_graph* g) { return (flat_delta(g) + 31) / 32 * 32; }
 
 bool flat_eligible(const wbc_gpu_graph* g) {
   // the ELL copy exists (packed slots, degree <= 8, mirror-image rows: the
@@ -274,8 +281,9 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
                          !g->skewed && g->n >= (1u << 18);
   if ((g->tune_flat > 0 || auto_flat) && flat_eligible(g)) {
     s.flat = true;
-    s.threads = kFlatT;
-    s.dyn_smem = wbc_dev::flat_dyn_smem(flat_hist_words(g), g->flat_ke);
+    s.threads = g->tune_flat_threads ? (g->tune_flat_threads <= 256 ? 256 : g->tune_flat_threads <= 512 ? 512 : 1024)
+                                     : kFlatT;
+    s.dyn_smem = wbc_dev::flat_dyn_smem(flat_delta_words(g), flat_buckets(g), g->flat_ke);
     return s;
   }
   const uint64_t n = g->n;
@@ -363,7 +371,7 @@ uint64_t ws_dcap(const wbc_gpu_graph* g) {
 uint64_t flat_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, wbc_dev::kFlatChunk); }
 uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
   const uint64_t ke = static_cast<uint64_t>(std::max(4, g->flat_ke));
-  return flat_ns(g) * (8 + 4 + 4 + 4 + 16 + 8 + 8 + 4 + 8 * ke);
+  return flat_ns(g) * (8 + 4 + 2 * 4 + 4 + 16 + 8 + 8 + 4 + 4 * ke + 2 * 4 * ke);
 }
 
 void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
@@ -379,9 +387,9 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   w.psig = reinterpret_cast<double*>(carve(ns * 8));
   w.pcoef = reinterpret_cast<double*>(carve(ns * 8));
   w.psucc = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
-  w.ent = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
+  w.ent = reinterpret_cast<uint32_t*>(carve(2 * ns * 4 * ke));  // two buffers (sweeper / workers)
   w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.ord_d = reinterpret_cast<uint32_t*>(carve(ns * 4));
+  w.ord_d = reinterpret_cast<uint32_t*>(carve(2 * ns * 4));
   w.mem = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q0 = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q1 = reinterpret_cast<uint32_t*>(carve(ns * 4));
@@ -392,7 +400,7 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   w.ell_eid = g->d_ell_eid;
   w.delta_w = flat_delta(g);
   w.buckets = flat_buckets(g);
-  w.hist_words = flat_hist_words(g);
+  w.delta_words = flat_delta_words(g);
 }
 
 uint64_t ws_per_slot(const wbc_gpu_graph* g, bool team, bool one_warp = false) {
@@ -461,11 +469,10 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   const uint64_t per_slot = shape.flat ? ws_flat_per_slot(g) : ws_per_slot(g, team, one_warp);
   int slots = 0;
   if (shape.flat) {
-    const void* f = reinterpret_cast<const void*>(g->flat_ke == 4 ? wbc_dev::bc_flat_kernel<kFlatT, 4>
-                                                                   : wbc_dev::bc_flat_kernel<kFlatT, 8>);
+    const void* f = reinterpret_cast<const void*>(pick_flat(shape.threads, g->flat_ke));
     WBC_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shape.dyn_smem)));
     int per_sm = 0;
-    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kFlatT, shape.dyn_smem));
+    WBC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, shape.threads, shape.dyn_smem));
     if (per_sm < 1) return set_error(WBC_E_CUDA, "flat kernel does not fit on an SM");
     slots = per_sm * g->sm_count;
   }
@@ -639,8 +646,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     rc = launch_strict(g, shape, slots, p, k, edge_bc, d_edge, strict_lanes, stream);
     if (rc) return rc;
   } else if (shape.flat) {
-    const auto fk = g->flat_ke == 4 ? wbc_dev::bc_flat_kernel<kFlatT, 4> : wbc_dev::bc_flat_kernel<kFlatT, 8>;
-    fk<<<slots, kFlatT, shape.dyn_smem, stream>>>(p, g->fw);
+    pick_flat(shape.threads, g->flat_ke)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p, g->fw);
     WBC_CUDA_TRY(cudaGetLastError());
   } else if (shape.cluster > 0) {
     // whole distance arrays of the few in-flight teams get evict-last
@@ -1141,6 +1147,7 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "fill") g->tune_fill = static_cast<int>(value);
   else if (k == "flat") g->tune_flat = static_cast<int>(value);
   else if (k == "flat_delta") g->tune_flat_delta = static_cast<uint32_t>(std::max<int64_t>(0, value));
+  else if (k == "flat_threads") g->tune_flat_threads = static_cast<int>(value);
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }
