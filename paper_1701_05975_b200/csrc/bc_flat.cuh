@@ -63,8 +63,16 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #define WBC_FLAT_RELAX_U 2
 #endif
 #ifndef WBC_FLAT_PRECHECK
-#define WBC_FLAT_PRECHECK 1
+#define WBC_FLAT_PRECHECK 0
 #endif
+#ifndef WBC_FLAT_PREFETCH
+#define WBC_FLAT_PREFETCH 0
+#endif
+constexpr bool kRelaxPrefetch = WBC_FLAT_PREFETCH;  // prefetch a pushed vertex's ELL row into L2
+#ifndef WBC_FLAT_SWEEPERS
+#define WBC_FLAT_SWEEPERS 1
+#endif
+constexpr int kSweepers = WBC_FLAT_SWEEPERS;  // sweeper warps per CTA (<= 3)
 constexpr int kRelaxU = WBC_FLAT_RELAX_U;            // near vertices per thread and step in A
 constexpr bool kRelaxPrecheck = WBC_FLAT_PRECHECK;   // gather before the atomicMin
 
@@ -131,9 +139,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Dynamic shared memory of bc_flat_kernel<T, KE>: the workers' window-sort
-// histogram, then the sweeper's bucket ring and its cp.async ring.
+// histogram, then per sweeper its bucket ring and cp.async ring.
 inline size_t flat_dyn_smem(uint32_t delta_words, uint32_t buckets, int ke) {
-  return (static_cast<size_t>(delta_words) + buckets + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke)) * 4;
+  return (static_cast<size_t>(delta_words) +
+          kSweepers * (buckets + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke))) * 4;
 }
 
 // ELL record of v: 2 KE words (slots, then keys two per word)
@@ -174,6 +183,129 @@ __device__ __forceinline__ void ell_keys(const FlatWs& w, uint32_t v, uint32_t (
 }
 __device__ __forceinline__ uint32_t* dist_of(uint2* dp, uint32_t v) { return reinterpret_cast<uint32_t*>(dp + v); }
 
+// The Eq. 4 threshold sweep of one source, run by one warp: ord_d / ent are
+// the source's sorted distances and sweep entries (reached positions);
+// bucket (B words) and the cp.async ring s_sd (kFlatRing * kFlatChunk) /
+// s_en (x KE) are the warp's shared memory.  Returns depth_per_source.
+// bucket[k & M] = 1 + the largest d(v) over inserted slots u->v with key k;
+// k is live at threshold tau iff that d(v) >= tau.  A slot's stale value
+// (key k - B) is always below tau + 1 (its d(v) < k - B < tau), so slots are
+// cleared only per source.
+template <int KE>
+__device__ __forceinline__ uint32_t flat_sweep(const uint32_t* __restrict__ ord_d, const uint32_t* __restrict__ ent,
+                                              uint32_t reached, uint32_t B, uint32_t* bucket, uint32_t* s_sd,
+                                              uint32_t* s_en, uint32_t lane) {
+  const uint32_t M = B - 1;
+  constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
+  static_assert(kFlatChunk >= 64, "a 64-position block spans at most two chunks");
+  for (uint32_t i = lane; i < B; i += 32) bucket[i] = 0;
+  auto stage = [&](uint32_t c) {  // chunk c -> ring slot c % kFlatRing
+    if (c * kFlatChunk < reached) {
+      const uint32_t sl = c % kFlatRing;
+      for (uint32_t k = lane; k < kFlatChunk / 4; k += 32)
+        cp_async16(s_sd + sl * kFlatChunk + 4 * k, ord_d + c * kFlatChunk + 4 * k);
+      for (uint32_t k = lane; k < kFlatChunk * KE / 4; k += 32)
+        cp_async16(s_en + sl * kFlatChunk * KE + 4 * k,
+                   ent + static_cast<uint64_t>(c) * kFlatChunk * KE + 4 * k);
+    }
+    cp_async_commit();
+  };
+  // chunks [cur, cur + kFlatRing) are issued; cur and cur + 1 are complete
+  uint32_t issued = 0, cur = 0;
+  for (; issued < static_cast<uint32_t>(kFlatRing); ++issued) stage(issued);
+  cp_async_wait<kFlatRing - 2>();
+  __syncwarp();
+  auto advance_to = [&](uint32_t q) {  // position q (only grows) moves the window
+    while (cur < q / kFlatChunk) {
+      __syncwarp();  // every lane is done with chunk cur's slot
+      ++cur;
+      stage(issued++);
+      cp_async_wait<kFlatRing - 2>();
+      __syncwarp();
+    }
+  };
+  // level 0 = {s}: insert its entries (d(s) = 0)
+  uint32_t newmin = kInfDist;  // smallest key inserted by the last level, live at its threshold
+  if (lane < KE) {
+    const uint32_t e = s_en[lane];
+    if (e) {
+      atomicMax(bucket + ((e & 0xFFFFu) & M), (e >> 16) + 1);
+      newmin = e & 0xFFFFu;  // d(v) = e >> 16 >= 1 = tau: live
+    }
+  }
+  newmin = __reduce_min_sync(0xffffffffu, newmin);
+  __syncwarp();
+  uint32_t tau = 1, pos = 1, levels = 1;
+  // the first 32 positions of the next level, loaded ahead of its threshold
+  auto load_step = [&](uint32_t q, uint32_t& d, uint32_t (&e)[KE]) {
+    const uint32_t qq = q + lane;
+    d = qq < reached ? s_sd[qq % kRingPos] : kInfDist;
+    const uint4* e4 = reinterpret_cast<const uint4*>(s_en + (qq % kRingPos) * KE);
+#pragma unroll
+    for (int h = 0; h < KE / 4; ++h) {
+      const uint4 t = e4[h];
+      e[4 * h] = t.x;
+      e[4 * h + 1] = t.y;
+      e[4 * h + 2] = t.z;
+      e[4 * h + 3] = t.w;
+    }
+  };
+  uint32_t pd, pe[KE];
+  advance_to(pos);
+  load_step(pos, pd, pe);
+  for (;;) {
+    // the next threshold: the first live key > tau in the ring, or newmin
+    uint32_t nxt = newmin;
+    for (uint32_t base = tau + 1; base < tau + B && base <= nxt; base += 32) {
+      const uint32_t k = base + lane;
+      const bool live = k < tau + B && bucket[k & M] >= tau + 1;
+      __syncwarp();  // orders the last level's inserts before the scans after this one
+      const uint32_t m = __ballot_sync(0xffffffffu, live);
+      if (m) {
+        nxt = min(nxt, base + __ffs(m) - 1);
+        break;
+      }
+    }
+    if (nxt == kInfDist) break;
+    // the new level: positions [pos, end) with d < nxt, 32 per step
+    uint32_t q = pos, lmin = kInfDist;
+    uint32_t d = pd, ex[KE];
+#pragma unroll
+    for (int x = 0; x < KE; ++x) ex[x] = pe[x];
+    for (;;) {
+      const bool in = d < nxt;  // d = kInfDist past the end
+      const uint32_t got = __popc(__ballot_sync(0xffffffffu, in));
+#pragma unroll
+      for (int x = 0; x < KE; ++x) {
+        const uint32_t dvp1 = d + (ex[x] >> 16) + 1;
+        const uint32_t key = d + (ex[x] & 0xFFFFu);
+        const bool v = in && ex[x] != 0u && dvp1 > nxt;
+        atomicMax(bucket + (key & M), v ? dvp1 : 0u);  // unconditional: no branch per entry
+        lmin = v ? min(lmin, key) : lmin;
+      }
+      q += got;
+      if (got < 32 || q >= reached) break;
+      advance_to(q);
+      load_step(q, d, ex);
+    }
+    newmin = __reduce_min_sync(0xffffffffu, lmin);
+    pos = q;
+    tau = nxt;
+    ++levels;
+    if (pos < reached) {
+      advance_to(pos);
+      load_step(pos, pd, pe);
+    } else {
+      pd = kInfDist;
+#pragma unroll
+      for (int x = 0; x < KE; ++x) pe[x] = 0;
+    }
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  return levels;
+}
+
 // Named barriers of bc_flat_kernel (0 is __syncthreads, unused in the loop):
 // 1 = the worker group (warps 1..), 2 / 3 = buffer 0 / 1 ready for the
 // sweeper, 4 / 5 = buffer 0 / 1 released by the sweeper.
@@ -185,27 +317,42 @@ template <int ID>
 __device__ __forceinline__ void nbar_arrive(int count) {
   asm volatile("bar.arrive %0, %1;" ::"n"(ID), "r"(count) : "memory");
 }
-// buffer b's ready (2 + b) / released (4 + b) barriers
-template <int BASE>
-__device__ __forceinline__ void buf_sync(uint32_t b, int count) {
-  if (b) nbar_sync<BASE + 1>(count); else nbar_sync<BASE>(count);
-}
-template <int BASE>
-__device__ __forceinline__ void buf_arrive(uint32_t b, int count) {
-  if (b) nbar_arrive<BASE + 1>(count); else nbar_arrive<BASE>(count);
+// Sweeper j's buffer parity p: ready barrier 2 + 4j + p (workers arrive,
+// the sweeper waits), released barrier 4 + 4j + p (the sweeper arrives, the
+// workers wait).  kSweepers <= 3 keeps every id below 16.
+template <bool READY>
+__device__ __forceinline__ void buf_bar(bool sync, uint32_t j, uint32_t par, int count) {
+  const uint32_t c = j * 2 + par;
+  constexpr int kB = READY ? 2 : 4;
+#define WBC_BUF_CASE(C)                                                   \
+  case C:                                                                 \
+    if (sync) nbar_sync<kB + 4 * ((C) / 2) + (C) % 2>(count);             \
+    else nbar_arrive<kB + 4 * ((C) / 2) + (C) % 2>(count);                \
+    break;
+  switch (c) {
+    WBC_BUF_CASE(0)
+    WBC_BUF_CASE(1)
+    WBC_BUF_CASE(2)
+    WBC_BUF_CASE(3)
+    WBC_BUF_CASE(4)
+    WBC_BUF_CASE(5)
+  }
+#undef WBC_BUF_CASE
 }
 
 template <int T, int KE>
 __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p, const FlatWs w) {
   static_assert(KE == 4 || KE == 8, "ELL row width");
-  constexpr uint32_t TG = T - 32;           // worker threads (warps 1..)
+  constexpr uint32_t kSW = kSweepers;       // sweeper warps (0 .. kSW - 1)
+  constexpr uint32_t TG = T - 32 * kSW;     // worker threads (the other warps)
+  constexpr int kBarN = TG + 32;            // threads on a ready / released barrier
   constexpr int kU = 2;                     // positions per thread in a pull block
   constexpr uint32_t kBlk = TG * kU;        // pull block (passes B and C)
   __shared__ unsigned long long s_src;
   __shared__ uint32_t s_ring[3][4];          // per-phase counters: [near, far, members, far min]
   __shared__ uint32_t s_warp[T / 32];
   __shared__ double s_blk[kBlk];             // the block's sigma (B) / coef (C); 0 = not final
-  __shared__ uint32_t s_sw[2][3];            // per sweep buffer: reached, source, exit
+  __shared__ uint32_t s_sw[kSW][2][3];       // per sweeper and buffer: reached, source, exit
   volatile double* const s_blk_v = s_blk;
   extern __shared__ uint32_t smem[];         // hist | buckets | sweep ring
   const GraphView& g = p.g;
@@ -220,138 +367,38 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
   uint32_t* const pinfo = w.pinfo + off;
   uint32_t* const psucc = w.psucc + off * KE;
   uint32_t* const hist = smem;
-  uint32_t* const bucket = smem + w.delta_words;
   const uint32_t wbits = g.wbits, wmask = g.wmask;
-  // the sweep inputs are double-buffered: buffer b of this slot
-  auto ord_d_of = [&](uint32_t b) { return w.ord_d + (2 * off + b * w.n_stride); };
-  auto ent_of = [&](uint32_t b) { return w.ent + (2 * off + b * w.n_stride) * KE; };
+  // the sweep inputs are double-buffered per sweeper: buffer (j, parity)
+  auto ord_d_of = [&](uint32_t j, uint32_t par) { return w.ord_d + (2 * kSW * off + (2 * j + par) * w.n_stride); };
+  auto ent_of = [&](uint32_t j, uint32_t par) {
+    return w.ent + (2 * kSW * off + (2 * j + par) * w.n_stride) * KE;
+  };
 
-  if (wid == 0) {
-    // ===================== the sweeper (warp 0): Eq. 4 thresholds of the
-    // source the workers finished last, while they run the next one.
-    // bucket[k & M] = 1 + the largest d(v) over inserted slots u->v with
-    // key k; k is live at threshold tau iff that d(v) >= tau.  A slot's
-    // stale value (key k - B) is always below tau + 1 (its d(v) < k - B <
-    // tau), so slots are cleared only per source.  Per level the scan for the
-    // next threshold and the level's position data (cp.async ring) are loaded
-    // together; the keys the level itself inserts enter the next threshold
-    // through a warp min in registers.
-    const uint32_t B = w.buckets, M = B - 1;
+  if (wid < kSW) {
+    // ===================== sweeper j (warp j): the Eq. 4 thresholds of the
+    // sources j, j + kSW, j + 2 kSW, ... this CTA runs, each while the
+    // workers run the following ones (one sweep takes about as long as a
+    // source's SSSP + sigma + delta, so kSW sweepers keep up).
+    const uint32_t j = wid, B = w.buckets;
+    uint32_t* const bucket = smem + w.delta_words + j * (B + kFlatRing * kFlatChunk * (1 + KE));
     uint32_t* const s_sd = bucket + B;
     uint32_t* const s_en = s_sd + kFlatRing * kFlatChunk;
-    constexpr uint32_t kRingPos = kFlatRing * kFlatChunk;
-    static_assert(kFlatChunk >= 64, "a 64-position block spans at most two chunks");
-    for (uint32_t j = 0;; ++j) {
-      const uint32_t b = j & 1;
-      buf_sync<2>(b, T);
-      if (s_sw[b][2]) break;
+    for (uint32_t m = 0;; ++m) {
+      const uint32_t par = m & 1;
+      buf_bar<true>(true, j, par, kBarN);
+      if (s_sw[j][par][2]) break;
       const unsigned long long t_sweep = clock64();
-      const uint32_t reached = s_sw[b][0], s_orig = s_sw[b][1];
-      const uint32_t* const ord_d = ord_d_of(b);
-      const uint32_t* const ent = ent_of(b);
-      for (uint32_t i = lane; i < B; i += 32) bucket[i] = 0;
-      auto stage = [&](uint32_t c) {  // chunk c -> ring slot c % kFlatRing
-        if (c * kFlatChunk < reached) {
-          const uint32_t sl = c % kFlatRing;
-          for (uint32_t k = lane; k < kFlatChunk / 4; k += 32)
-            cp_async16(s_sd + sl * kFlatChunk + 4 * k, ord_d + c * kFlatChunk + 4 * k);
-          for (uint32_t k = lane; k < kFlatChunk * KE / 4; k += 32)
-            cp_async16(s_en + sl * kFlatChunk * KE + 4 * k,
-                       ent + static_cast<uint64_t>(c) * kFlatChunk * KE + 4 * k);
-        }
-        cp_async_commit();
-      };
-      // chunks [cur, cur + kFlatRing) are issued; cur and cur + 1 are complete
-      uint32_t issued = 0, cur = 0;
-      for (; issued < static_cast<uint32_t>(kFlatRing); ++issued) stage(issued);
-      cp_async_wait<kFlatRing - 2>();
-      __syncwarp();
-      auto advance_to = [&](uint32_t q) {  // position q (only grows) moves the window
-        while (cur < q / kFlatChunk) {
-          __syncwarp();  // every lane is done with chunk cur's slot
-          ++cur;
-          stage(issued++);
-          cp_async_wait<kFlatRing - 2>();
-          __syncwarp();
-        }
-      };
-      // level 0 = {s}: insert its entries (d(s) = 0)
-      uint32_t newmin = kInfDist;  // smallest key inserted by the last level, live at its threshold
-      if (lane < KE) {
-        const uint32_t e = s_en[lane];
-        if (e) {
-          atomicMax(bucket + ((e & 0xFFFFu) & M), (e >> 16) + 1);
-          newmin = e & 0xFFFFu;  // d(v) = e >> 16 >= 1 = tau: live
-        }
-      }
-      newmin = __reduce_min_sync(0xffffffffu, newmin);
-      __syncwarp();
-      uint32_t tau = 1, pos = 1, levels = 1;
-      for (;;) {
-        // the next threshold: the first live key > tau in the ring, or newmin
-        uint32_t nxt = newmin;
-        for (uint32_t base = tau + 1; base < tau + B && base <= nxt; base += 32) {
-          const uint32_t k = base + lane;
-          const bool live = k < tau + B && bucket[k & M] >= tau + 1;
-          const uint32_t m = __ballot_sync(0xffffffffu, live);
-          if (m) {
-            nxt = min(nxt, base + __ffs(m) - 1);
-            break;
-          }
-        }
-        if (nxt == kInfDist) break;
-        // the new level: positions [pos, end) with d < nxt, 64 per block
-        uint32_t q = pos, lmin = kInfDist;
-        while (q < reached) {
-          advance_to(q);
-          uint32_t d[2], e[2][KE];
-          bool in[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t qq = q + 32 * h + lane;
-            in[h] = qq < reached;
-            d[h] = in[h] ? s_sd[qq % kRingPos] : kInfDist;
-            const uint32_t* eq = s_en + (qq % kRingPos) * KE;
-#pragma unroll
-            for (int x = 0; x < KE; ++x) e[h][x] = in[h] ? eq[x] : 0u;
-          }
-          uint32_t got = 0;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            in[h] = in[h] && d[h] < nxt;
-            got += __popc(__ballot_sync(0xffffffffu, in[h]));  // a prefix: positions are sorted
-            if (!in[h]) continue;
-#pragma unroll
-            for (int x = 0; x < KE; ++x) {
-              const uint32_t ex = e[h][x];
-              const uint32_t dvp1 = d[h] + (ex >> 16) + 1;  // d(v) + 1
-              if (ex && dvp1 > nxt) {  // dead entries (v already settled) never matter again
-                const uint32_t key = d[h] + (ex & 0xFFFFu);
-                atomicMax(bucket + (key & M), dvp1);
-                lmin = min(lmin, key);
-              }
-            }
-          }
-          q += got;
-          if (got < 64) break;
-        }
-        newmin = __reduce_min_sync(0xffffffffu, lmin);
-        __syncwarp();  // this level's inserts are visible to the scans after the next one
-        pos = q;
-        tau = nxt;
-        ++levels;
-      }
-      cp_async_wait<0>();
-      __syncwarp();
+      const uint32_t reached = s_sw[j][par][0], s_orig = s_sw[j][par][1];
+      const uint32_t levels = flat_sweep<KE>(ord_d_of(j, par), ent_of(j, par), reached, B, bucket, s_sd, s_en, lane);
       if (lane == 0 && p.depth) p.depth[s_orig] = levels;
       if (p.prof && lane == 0) atomicAdd(p.prof + kProfCyclesSettle, clock64() - t_sweep);
-      buf_arrive<4>(b, T);  // buffer b is free again
+      buf_bar<false>(false, j, par, kBarN);  // buffer (j, par) is free again
     }
     return;
   }
 
-  // ======================= the workers (warps 1..): SSSP, sigma, delta
-  const uint32_t gt = tid - 32, gw = wid - 1;  // worker thread / warp index
+  // ======================= the workers (warps kSW..): SSSP, sigma, delta
+  const uint32_t gt = tid - 32 * kSW, gw = wid - kSW;  // worker thread / warp index
   auto gsync = [&]() { nbar_sync<1>(TG); };
   auto gsync_or = [&](uint32_t pred) { return bar_or(pred, 1, TG); };
   // p.prof: per-phase SM cycles of worker 0 (init -> kProfCyclesInit, A ->
@@ -371,21 +418,25 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     if (gt == 0) s_src = atomicAdd(p.counter, 1ULL);
     gsync();
     const unsigned long long idx = s_src;
-    const uint32_t b = nsrc & 1;
+    // source nsrc goes to sweeper sj, its m-th, buffer parity sp
+    const uint32_t sj = nsrc % kSW, sm_ = nsrc / kSW, sp = sm_ & 1;
     if (idx >= p.k) {
-      // release the sweeper: consume its last releases, signal the exit
-      if (nsrc >= 2) buf_sync<4>(b, T);
-      if (gt == 0) s_sw[b][2] = 1;
-      buf_arrive<2>(b, T);
-      if (nsrc >= 1) buf_sync<4>(b ^ 1, T);
+      // release every sweeper: consume its outstanding releases, signal the exit
+      for (uint32_t jj = 0; jj < kSW; ++jj) {
+        const uint32_t cnt = (nsrc + kSW - 1 - jj) / kSW;  // sources sweeper jj got
+        if (cnt >= 2) buf_bar<false>(true, jj, cnt & 1, kBarN);  // sweep cnt - 2 released
+        if (gt == 0) s_sw[jj][cnt & 1][2] = 1;
+        buf_bar<true>(false, jj, cnt & 1, kBarN);
+        if (cnt >= 1) buf_bar<false>(true, jj, (cnt - 1) & 1, kBarN);  // sweep cnt - 1 released
+      }
       break;
     }
     const uint32_t s_orig = p.sources ? __ldg(p.sources + idx) : static_cast<uint32_t>(p.src_base + idx);
     const uint32_t s = __ldg(p.inv + s_orig);
     tick(-1);
-    if (nsrc >= 2) buf_sync<4>(b, T);  // the sweeper is done with buffer b (source nsrc - 2)
-    uint32_t* const ord_d = ord_d_of(b);
-    uint32_t* const ent = ent_of(b);
+    if (sm_ >= 2) buf_bar<false>(true, sj, sp, kBarN);  // sweeper sj is done with this buffer (its m - 2)
+    uint32_t* const ord_d = ord_d_of(sj, sp);
+    uint32_t* const ent = ent_of(sj, sp);
 
     // ---- init: every word (infinite distance, position 0)
     {
@@ -466,6 +517,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
                 // reads the current distance); members are appended once, at
                 // the crossing below the window end
                 nn[atomicAdd(&R[0], 1u)] = u;
+                if constexpr (kRelaxPrefetch) asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_rec<KE>(w, u)));
                 if (old[j][x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u;
               } else if (old[j][x] == kInfDist) {
                 fq[far_len + atomicAdd(&R[1], 1u)] = u;
@@ -473,6 +525,9 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
             }
         }
         gsync();
+#ifdef WBC_FLAT_SSSP_PROF
+        if (p.prof && gt == 0) atomicAdd(p.prof + kProfNearScanned, static_cast<unsigned long long>(near_len));
+#endif
         near_len = R[0];
         far_len += R[1];
         mem_len += R[2];
@@ -568,6 +623,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           if (u[j] == kInfDist || du[j] < thr32) continue;  // joined an earlier window: sorted already
           if (du[j] < tn32) {
             nq[atomicAdd(&R[0], 1u)] = u[j];
+            if constexpr (kRelaxPrefetch) asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_rec<KE>(w, u[j])));
             mem[atomicAdd(&R[2], 1u)] = u[j];
           } else {
             fq2[atomicAdd(&R[1], 1u)] = u[j];
@@ -699,11 +755,11 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     tick(kProfCyclesThreshold);
     // hand the distances and entries to the sweeper (buffer b)
     if (gt == 0) {
-      s_sw[b][0] = reached;
-      s_sw[b][1] = s_orig;
-      s_sw[b][2] = 0;
+      s_sw[sj][sp][0] = reached;
+      s_sw[sj][sp][1] = s_orig;
+      s_sw[sj][sp][2] = 0;
     }
-    buf_arrive<2>(b, T);
+    buf_bar<true>(false, sj, sp, kBarN);
 
     // ---- C. delta in reverse distance order, a block of kBlk positions at a
     // time: successors in later blocks are final (global pcoef), those inside

@@ -239,7 +239,7 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g);
 LaunchShape pick_shape(wbc_gpu_graph* g);
 
 // bc_flat_kernel: CTA size (two CTAs per SM: its phases are latency-bound)
-constexpr int kFlatT = 512;  // default; set_param("flat_threads", 256 | 512 | 1024)
+constexpr int kFlatT = 1024;  // default; set_param("flat_threads", 256 | 512 | 1024)
 
 using FlatFn = void (*)(const wbc_dev::RunParams, const wbc_dev::FlatWs);
 FlatFn pick_flat(int threads, int ke) {
@@ -371,7 +371,8 @@ uint64_t ws_dcap(const wbc_gpu_graph* g) {
 uint64_t flat_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, wbc_dev::kFlatChunk); }
 uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
   const uint64_t ke = static_cast<uint64_t>(std::max(4, g->flat_ke));
-  return flat_ns(g) * (8 + 4 + 2 * 4 + 4 + 16 + 8 + 8 + 4 + 4 * ke + 2 * 4 * ke);
+  const uint64_t bufs = 2 * wbc_dev::kSweepers;  // sweep inputs: two buffers per sweeper warp
+  return flat_ns(g) * (8 + 4 + bufs * 4 + 4 + 16 + 8 + 8 + 4 + 4 * ke + bufs * 4 * ke);
 }
 
 void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
@@ -387,9 +388,10 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   w.psig = reinterpret_cast<double*>(carve(ns * 8));
   w.pcoef = reinterpret_cast<double*>(carve(ns * 8));
   w.psucc = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
-  w.ent = reinterpret_cast<uint32_t*>(carve(2 * ns * 4 * ke));  // two buffers (sweeper / workers)
+  const uint64_t bufs = 2 * wbc_dev::kSweepers;
+  w.ent = reinterpret_cast<uint32_t*>(carve(bufs * ns * 4 * ke));  // two buffers per sweeper
   w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));
-  w.ord_d = reinterpret_cast<uint32_t*>(carve(2 * ns * 4));
+  w.ord_d = reinterpret_cast<uint32_t*>(carve(bufs * ns * 4));
   w.mem = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q0 = reinterpret_cast<uint32_t*>(carve(ns * 4));
   w.q1 = reinterpret_cast<uint32_t*>(carve(ns * 4));
