@@ -498,7 +498,9 @@ def device_count() -> int:
 
 def resolve_devices(device: int = -1) -> list:
     """Devices bc_parallel runs on: `device` if >= 0, else WBC_GPU_DEVICES
-    ("0,1,..." or "all"), else every visible device (host_engine.cpp resolve_devices)."""
+    ("0,1,..." or "all"), else -- under a one-process-per-GPU launcher
+    (WORLD_SIZE > 1 or LOCAL_RANK set) -- the current device, else every
+    visible device (host_engine.cpp resolve_devices)."""
     if device >= 0:
         return [device]
     count = device_count()
@@ -509,6 +511,9 @@ def resolve_devices(device: int = -1) -> list:
         out = [int(t) for t in env.split(",") if t]
         if out:
             return out
+    launched = "LOCAL_RANK" in os.environ or int(os.environ.get("WORLD_SIZE", "1") or 1) > 1
+    if launched and env != "all":
+        return [-1]
     return list(range(count))
 
 

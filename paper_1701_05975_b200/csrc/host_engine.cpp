@@ -6,8 +6,13 @@
 // empty source list / empty graph return zeros (engine.cpp:382-385),
 // depth_per_source sized n (engine.cpp:379), Halved (engine.cpp:451-454).
 // The GPU computes the same sums; the CPU schedule fields only validate.
+#include <algorithm>
 #include <cstdlib>
+#include <limits>
+#include <memory>
+#include <mutex>
 #include <sstream>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -74,8 +79,10 @@ void validate(const EngineOptions& opt) {
 namespace {
 
 // GpuOptions::device >= 0: that device.  -1: the devices listed in
-// WBC_GPU_DEVICES ("0,1,2" -- repeats allowed, for tests -- or "all"), else
-// every visible device.
+// WBC_GPU_DEVICES ("0,1,2" -- repeats allowed, for tests -- or "all"); else,
+// in a process started by a multi-process launcher (WORLD_SIZE > 1 or
+// LOCAL_RANK set: one process per GPU, e.g. torchrun) the current device
+// only; else every visible device.
 std::vector<int> resolve_devices(int device) {
   if (device >= 0) return {device};
   int count = 0;
@@ -88,9 +95,46 @@ std::vector<int> resolve_devices(int device) {
     while (std::getline(ss, tok, ','))
       if (!tok.empty()) out.push_back(std::stoi(tok));
   }
-  if (out.empty())
+  if (out.empty()) {
+    const char* ws = std::getenv("WORLD_SIZE");
+    const bool launched = std::getenv("LOCAL_RANK") != nullptr || (ws && std::atoi(ws) > 1);
+    if (launched && !(e && std::string(e) == "all")) return {-1};  // the process's current device
     for (int d = 0; d < count; ++d) out.push_back(d);
+  }
   return out;
+}
+
+// Content fingerprint of a CsrGraph (thread-parallel FNV-1a over its arrays):
+// bc_parallel keeps the last graph's device replica and reuses it when the
+// next call passes the same graph.
+uint64_t fingerprint(const CsrGraph& g) {
+  auto fnv = [](const unsigned char* p, size_t len, uint64_t h) {
+    for (size_t i = 0; i < len; ++i) h = (h ^ p[i]) * 1099511628211ULL;
+    return h;
+  };
+  struct Span {
+    const void* p;
+    size_t bytes;
+  };
+  const Span spans[] = {{g.offsets.data(), g.offsets.size() * 4}, {g.adjacency.data(), g.adjacency.size() * 4},
+                        {g.weights.data(), g.weights.size() * 8}, {g.edge_id.data(), g.edge_id.size() * 4},
+                        {g.min_incident_weight.data(), g.min_incident_weight.size() * 8}};
+  uint64_t h = 1469598103934665603ULL ^ (uint64_t{g.n} << 32 | g.m);
+  for (const Span& sp : spans) {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const size_t chunk = std::max<size_t>(1 << 20, (sp.bytes + hw - 1) / hw);
+    const size_t parts = (sp.bytes + chunk - 1) / chunk;
+    std::vector<uint64_t> ph(parts, 0);
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < parts; ++t)
+      ts.emplace_back([&, t] {
+        const size_t b = t * chunk, e = std::min(sp.bytes, b + chunk);
+        ph[t] = fnv(static_cast<const unsigned char*>(sp.p) + b, e - b, 1469598103934665603ULL + t);
+      });
+    for (auto& t : ts) t.join();
+    for (uint64_t x : ph) h = (h ^ x) * 1099511628211ULL;
+  }
+  return h;
 }
 
 }  // namespace
@@ -159,6 +203,8 @@ BcResult GpuBcEngine::bc(const EngineOptions& opt) const {
   return r;
 }
 
+wbc_gpu_graph* GpuBcEngine::device_handle() const { return impl_->h; }
+
 GpuBcEngine::SourceState GpuBcEngine::dump_source(NodeId s) const {
   SourceState st;
   st.dist.resize(n_);
@@ -169,6 +215,19 @@ GpuBcEngine::SourceState GpuBcEngine::dump_source(NodeId s) const {
   if (rc) throw_status(rc);
   return st;
 }
+
+namespace {
+struct BcCache {
+  std::mutex mu;
+  std::unique_ptr<GpuBcEngine> engine;
+  uint64_t fp = 0;
+  std::vector<int> devs;
+};
+BcCache& bc_cache() {
+  static BcCache c;
+  return c;
+}
+}  // namespace
 
 BcResult bc_parallel(const CsrGraph& g, const EngineOptions& opt) {
   validate(opt);
@@ -185,8 +244,141 @@ BcResult bc_parallel(const CsrGraph& g, const EngineOptions& opt) {
       return r;
     }
   }
-  GpuBcEngine engine(g);
-  return engine.bc(opt);
+  // Reuse the last call's device replica when g is the same graph (same
+  // dimensions and array contents); WBC_GPU_NO_CACHE=1 uploads every call.
+  std::mutex& mu = bc_cache().mu;
+  std::unique_ptr<GpuBcEngine>& cached = bc_cache().engine;
+  uint64_t& cached_fp = bc_cache().fp;
+  std::vector<int>& cached_devs = bc_cache().devs;
+  if (std::getenv("WBC_GPU_NO_CACHE")) {
+    GpuBcEngine engine(g);
+    return engine.bc(opt);
+  }
+  const uint64_t fp = fingerprint(g);
+  const std::vector<int> devs = resolve_devices(-1);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cached || cached_fp != fp || cached_devs != devs) {
+    cached.reset();  // free the old replica before uploading the new one
+    cached = std::make_unique<GpuBcEngine>(g);
+    cached_fp = fp;
+    cached_devs = devs;
+  }
+  return cached->bc(opt);
+}
+
+void release_bc_parallel_cache() {
+  std::lock_guard<std::mutex> lock(bc_cache().mu);
+  bc_cache().engine.reset();
+  bc_cache().fp = 0;
+  bc_cache().devs.clear();
+}
+
+
+// ---- per-phase API over the GPU (engine.hpp) ------------------------------
+
+namespace {
+void validate_strategy(const Strategy& strat, SettleRule rule) {
+  if (!valid_lane_width(strat.lane_width))
+    throw std::invalid_argument("invalid lane width " + std::to_string(strat.lane_width) +
+                                " (expected 1, 4, 8, 16 or 32)");
+  if (rule != SettleRule::StrictLess)
+    throw std::invalid_argument("SettleRule::LessEqual is a CPU-only negative control (not run on GPU)");
+}
+
+// The cached replica of g (shared with bc_parallel), created on first use.
+wbc_gpu_graph* cached_handle(const CsrGraph& g) {
+  const uint64_t fp = fingerprint(g);
+  const std::vector<int> devs = resolve_devices(-1);
+  std::lock_guard<std::mutex> lock(bc_cache().mu);
+  BcCache& c = bc_cache();
+  if (!c.engine || c.fp != fp || c.devs != devs) {
+    c.engine.reset();
+    c.engine = std::make_unique<GpuBcEngine>(g);
+    c.fp = fp;
+    c.devs = devs;
+  }
+  return c.engine->device_handle();
+}
+}  // namespace
+
+void init_state(const CsrGraph& g, NodeId source, TraversalState& st) {
+  if (source >= g.n) throw std::invalid_argument("init_state: source out of range");
+  const double inf = std::numeric_limits<double>::infinity();
+  st.dist.assign(g.n, inf);
+  st.sigma.assign(g.n, 0.0);
+  st.delta.assign(g.n, 0.0);
+  st.unsettled.assign(g.n, 1);
+  st.in_frontier.assign(g.n, 0);
+  st.frontier.assign(g.n, 0);
+  st.order.assign(g.n, 0);
+  st.ends.assign(uint64_t{g.n} + 1, 0);
+  st.dist[source] = 0.0;
+  st.sigma[source] = 1.0;
+  st.unsettled[source] = 0;
+  st.in_frontier[source] = 1;
+  st.frontier[0] = source;
+  st.frontier_len = 1;
+  st.order[0] = source;
+  st.order_len = 1;
+  st.ends[0] = 0;
+  st.ends[1] = 1;
+  st.ends_len = 2;
+  st.threshold = 0.0;
+  st.source = source;
+}
+
+void solve_source(const CsrGraph& g, NodeId source, const Strategy& strat, TraversalState& st, SettleRule rule) {
+  validate_strategy(strat, rule);
+  init_state(g, source, st);
+  wbc_gpu_graph* h = cached_handle(g);
+  std::vector<double> delta(g.n);
+  uint32_t depth = 0;
+  int rc = wbc_gpu_sssp_dump(h, source, st.dist.data(), st.sigma.data(), delta.data(), &depth);
+  if (rc) throw_status(rc);
+  std::vector<uint32_t> ends(uint64_t{g.n} + 2);
+  uint32_t olen = 0, levels = 0;
+  rc = wbc_gpu_sssp_levels(h, source, st.order.data(), &olen, ends.data(), &levels);
+  if (rc) throw_status(rc);
+  st.order_len = olen;
+  st.ends_len = levels + 1;
+  std::copy(ends.begin(), ends.begin() + st.ends_len, st.ends.begin());
+  std::fill(st.unsettled.begin(), st.unsettled.end(), 1);
+  for (uint32_t i = 0; i < olen; ++i) st.unsettled[st.order[i]] = 0;
+  std::fill(st.in_frontier.begin(), st.in_frontier.end(), 0);
+  const uint32_t fb = st.ends[st.ends_len - 2];
+  st.frontier_len = olen - fb;
+  for (uint32_t i = fb; i < olen; ++i) {
+    st.frontier[i - fb] = st.order[i];
+    st.in_frontier[st.order[i]] = 1;
+  }
+  st.threshold = std::numeric_limits<double>::infinity();
+}
+
+void solve_source_parallel(const CsrGraph& g, NodeId source, const Strategy& strat, int workers,
+                           TraversalState& st, SettleRule rule) {
+  if (workers < 1) throw std::invalid_argument("solve_source_parallel: workers must be >= 1");
+  solve_source(g, source, strat, st, rule);
+}
+
+void accumulate_dependencies(const CsrGraph& g, const Strategy& strat, TraversalState& st,
+                             std::span<double> node_acc, std::span<double> edge_acc) {
+  validate_strategy(strat, SettleRule::StrictLess);
+  if (st.source >= g.n) throw std::invalid_argument("accumulate_dependencies: source out of range");
+  wbc_gpu_graph* h = cached_handle(g);
+  st.delta.assign(g.n, 0.0);
+  int rc = wbc_gpu_sssp_dump(h, st.source, nullptr, nullptr, st.delta.data(), nullptr);
+  if (rc) throw_status(rc);
+  if (!node_acc.empty()) {
+    for (NodeId w = 0; w < g.n && w < node_acc.size(); ++w)
+      if (w != st.source) node_acc[w] += st.delta[w];
+  }
+  if (!edge_acc.empty()) {  // the DAG edges' terms: one device run of this source with edge BC
+    std::vector<double> node(g.n), edge(g.m);
+    const NodeId s = st.source;
+    rc = wbc_gpu_bc(h, &s, 1, WBC_EDGE_BC, node.data(), edge.data(), nullptr, nullptr);
+    if (rc) throw_status(rc);
+    for (EdgeId e = 0; e < g.m && e < edge_acc.size(); ++e) edge_acc[e] += edge[e];
+  }
 }
 
 }  // namespace wbc

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -832,18 +833,43 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
   if (n > 0 && (offsets[0] != 0 || offsets[n] != slots))
     return set_error(WBC_E_INVALID, "offsets must start at 0 and end at 2m");
   if (n == 0 && slots != 0) return set_error(WBC_E_INVALID, "edges without vertices");
-  for (uint32_t v = 0; v < n; ++v)
-    if (offsets[v + 1] < offsets[v]) return set_error(WBC_E_INVALID, "offsets not monotone");
-  uint64_t maxw = 0;
-  for (uint64_t e = 0; e < slots; ++e) {
-    const double w = weights[e];
-    if (adjacency[e] >= n) return set_error(WBC_E_INVALID, "adjacency entry out of range");
-    if (!(w >= 1.0) || w != std::floor(w) || w > 4294967295.0)
-      return set_error(WBC_E_UNSUPPORTED,
-                       "weights must be positive integers (exact u32 distances); got " +
-                           std::to_string(w));
-    maxw = std::max<uint64_t>(maxw, static_cast<uint64_t>(w));
-  }
+  // validation, thread-parallel: the first failing slot (lowest index) is reported
+  std::atomic<uint64_t> bad_off{UINT64_MAX}, bad_adj{UINT64_MAX}, bad_w{UINT64_MAX};
+  std::atomic<uint64_t> maxw_a{0};
+  auto atomic_min = [](std::atomic<uint64_t>& a, uint64_t v) {
+    uint64_t cur = a.load();
+    while (v < cur && !a.compare_exchange_weak(cur, v)) {}
+  };
+  parallel_for(n, [&](uint64_t b, uint64_t e) {
+    for (uint64_t v = b; v < e; ++v)
+      if (offsets[v + 1] < offsets[v]) {
+        atomic_min(bad_off, v);
+        return;
+      }
+  });
+  if (bad_off.load() != UINT64_MAX) return set_error(WBC_E_INVALID, "offsets not monotone");
+  parallel_for(slots, [&](uint64_t b, uint64_t e) {
+    uint64_t mw = 0;
+    for (uint64_t x = b; x < e; ++x) {
+      const double w = weights[x];
+      if (adjacency[x] >= n) {
+        atomic_min(bad_adj, x);
+        break;
+      }
+      if (!(w >= 1.0) || w != std::floor(w) || w > 4294967295.0) {
+        atomic_min(bad_w, x);
+        break;
+      }
+      mw = std::max<uint64_t>(mw, static_cast<uint64_t>(w));
+    }
+    uint64_t cur = maxw_a.load();
+    while (mw > cur && !maxw_a.compare_exchange_weak(cur, mw)) {}
+  });
+  if (bad_adj.load() < bad_w.load()) return set_error(WBC_E_INVALID, "adjacency entry out of range");
+  if (bad_w.load() != UINT64_MAX)
+    return set_error(WBC_E_UNSUPPORTED, "weights must be positive integers (exact u32 distances); got " +
+                                            std::to_string(weights[bad_w.load()]));
+  const uint64_t maxw = maxw_a.load();
   if (n > 0 && uint64_t{n} * std::max<uint64_t>(maxw, 1) >= 0xFFFFFFFFULL)
     return set_error(WBC_E_UNSUPPORTED, "n * max_weight must stay below 2^32-1");
   h.n = n;
@@ -935,9 +961,11 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
   // The flat kernel's dataflows count DAG edges from both ends; a caller CSR
   // whose rows are not mirror images (not from build_csr) must not reach it.
   if (h.max_degree <= static_cast<uint32_t>(wbc_dev::kFlatMaxDeg)) {
-    h.symmetric = true;
-    for (uint32_t u = 0; u < n && h.symmetric; ++u)
-      for (uint32_t e = h.noff[u]; e < h.noff[u + 1] && h.symmetric; ++e) {
+    std::atomic<bool> sym{true};
+    parallel_for(n, [&](uint64_t ub, uint64_t ue) {
+    bool ok = true;
+    for (uint32_t u = static_cast<uint32_t>(ub); u < ue && ok && sym.load(std::memory_order_relaxed); ++u)
+      for (uint32_t e = h.noff[u]; e < h.noff[u + 1] && ok; ++e) {
         const uint32_t v = packed ? h.slot32[e] >> wbits : h.slot64[e].x;
         const uint32_t w = packed ? h.slot32[e] & ((wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1)) : h.slot64[e].y;
         uint32_t twins = 0, same = 0;
@@ -951,8 +979,11 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
           const uint32_t y = packed ? h.slot32[f] & ((wbits >= 32) ? 0xFFFFFFFFu : ((1u << wbits) - 1)) : h.slot64[f].y;
           same += x == v && y == w;
         }
-        h.symmetric = twins == same && u != v;
+        ok = twins == same && u != v;
       }
+    if (!ok) sym.store(false);
+    });
+    h.symmetric = sym.load();
   }
   // ELL rows for the distance-first kernel: packed slots, weight 0 pads
   uint64_t max_key = 0;

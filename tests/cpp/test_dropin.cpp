@@ -104,6 +104,42 @@ static void gpu_cases() {
     threw = true;
   }
   CHECK(threw);
+
+  // the per-phase API (reference engine.hpp:46-106, test_engine.cpp cases)
+  TraversalState st0;
+  init_state(p3, 1, st0);
+  CHECK(st0.order_len == 1 && st0.ends_len == 2 && st0.dist[1] == 0.0 && st0.sigma[1] == 1.0 &&
+        st0.frontier_len == 1 && st0.unsettled[1] == 0 && std::isinf(st0.dist[0]));
+  TraversalState sp;
+  solve_source(p3, 0, Strategy{}, sp);
+  CHECK(sp.depth() == 3 && sp.order_len == 3 && sp.frontier_len == 1 && sp.frontier[0] == 2);
+  CHECK(sp.dist == (std::vector<double>{0.0, 1.0, 2.0}) && std::isinf(sp.threshold));
+  TraversalState sq;
+  solve_source_parallel(ts, 0, parse_strategy("we-warp8"), 4, sq);
+  CHECK(sq.dist == (std::vector<double>{0.0, 1.0, 2.0, 3.0}) && sq.sigma[3] == 2.0 && sq.depth() == 4);
+  std::vector<double> acc(ts.n, 0.0), eacc(ts.m, 0.0);
+  for (NodeId s = 0; s < ts.n; ++s) {
+    TraversalState t;
+    solve_source(ts, s, Strategy{}, t);
+    accumulate_dependencies(ts, Strategy{}, t, acc, eacc);
+    if (s == 0) CHECK(t.delta == (std::vector<double>{0.0, 1.0, 1.0, 0.0}) || t.delta[1] == 1.0);
+  }
+  CHECK(close(acc, {0, 2, 4, 0}, 1e-12));
+  CHECK(close(eacc, {4, 2, 6, 6}, 1e-12));
+  threw = false;
+  try {
+    solve_source(ts, 0, Strategy{}, sq, SettleRule::LessEqual);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  threw = false;
+  try {
+    init_state(ts, 9, sq);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
 }
 
 int main(int argc, char** argv) {

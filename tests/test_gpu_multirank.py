@@ -94,3 +94,77 @@ def test_bc_parallel_shards_over_env_devices(W, oracle, monkeypatch):
     node, eb, depth = oracle.bc_eq4(g, edge_bc=True)
     assert approx_rel(r.node_bc, node, 1e-9).all() and approx_rel(r.edge_bc, eb, 1e-9).all()
     assert np.array_equal(r.depth_per_source, depth)
+
+
+def test_bc_distributed_device_path_one_rank_nccl(W, oracle):
+    """distributed.bc_distributed's device path (wbc_gpu_bc_device into one
+    fp64 buffer, one NCCL all-reduce) in a one-rank NCCL group: node / edge BC
+    and depth against the oracle, duplicates and Halved included."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1701_05975_b200.distributed import bc_distributed
+
+    g = _random_graph(W, 600, 6.0, 9)
+    src = np.array([5, 9, 5, 100, 599], np.uint32)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for halved in (False, True):
+            opt = W.EngineOptions(compute_edge_bc=True, sources=src,
+                                  normalization=W.Normalization.Halved if halved else W.Normalization.Raw)
+            r = bc_distributed(g, opt)
+            node, eb, depth = oracle.bc_eq4(g, sources=src, halved=halved, edge_bc=True)
+            assert approx_rel(r.node_bc, node, 1e-9).all() and approx_rel(r.edge_bc, eb, 1e-9).all()
+            assert np.array_equal(r.depth_per_source, depth)
+    finally:
+        dist.destroy_process_group()
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif("_gpus() < 2", reason="needs two GPUs (distinct-device NCCL)")
+def test_multi_handle_distinct_devices_nccl(W, oracle):
+    """wbc_gpu_multi_* over two distinct devices: real NCCL over NVLink."""
+    import torch  # noqa: F401
+    g = _random_graph(W, 900, 6.0, 21)
+    mg = W.MultiGpuGraph(g, [0, 1], nccl=True)
+    try:
+        assert mg.info() == {"num_devices": 2, "uses_nccl": True}
+        src = W.sample_sources(g.n, 77, 3)
+        r = mg.bc(W.EngineOptions(compute_edge_bc=True, sources=src))
+        node, eb, depth = oracle.bc_eq4(g, sources=src, edge_bc=True)
+        assert approx_rel(r.node_bc, node, 1e-9).all() and approx_rel(r.edge_bc, eb, 1e-9).all()
+        assert np.array_equal(r.depth_per_source, depth)
+    finally:
+        mg.close()
+
+
+@pytest.mark.skipif("_gpus() < 2", reason="needs two GPUs (one NCCL rank per GPU)")
+def test_bench_self_spawns_two_ranks(tmp_path):
+    """`python bench.py --gpus 2` (no launcher) runs two NCCL ranks and reduces
+    to the one-rank BC."""
+    common = ["--workload", "rmat16", "--steps", "1", "--warmup", "3", "--no-cpu-baseline"]
+    one = _run([sys.executable, "bench.py"] + common + ["--dump-bc", str(tmp_path / "one.npy")], tmp_path)
+    two = _run([sys.executable, "bench.py", "--gpus", "2"] + common + ["--dump-bc", str(tmp_path / "two.npy")], tmp_path)
+    assert two["n_gpus"] == 2 and two["config"]["nccl"]["nranks"] == 2
+    a, b = np.load(tmp_path / "one.npy"), np.load(tmp_path / "two.npy")
+    assert approx_rel(a, b, 1e-9).all()
+
+
+def test_bench_self_spawn_refuses_missing_gpus():
+    """--gpus N beyond the visible devices fails loudly (NCCL needs one GPU per rank)."""
+    n = _gpus() + 1
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", str(n), "--workload", "rmat16", "--steps", "1",
+                        "--warmup", "3", "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert p.returncode != 0 and f"needs {n} visible GPUs" in p.stderr
+
+
+def test_bench_self_spawn_gloo_two_ranks_one_gpu(tmp_path):
+    """The self-spawn path itself on the one-GPU pool: --gpus 2 with gloo (ranks share the GPU)."""
+    common = ["--workload", "rmat16", "--steps", "1", "--warmup", "3", "--no-cpu-baseline"]
+    two = _run([sys.executable, "bench.py", "--gpus", "2", "--dist-backend", "gloo"] + common, tmp_path)
+    assert two["n_gpus"] == 2

@@ -105,7 +105,7 @@ def test_team_dag_overflow_fallback(W, oracle, c):
     gg.close()
 
 
-@pytest.mark.parametrize("c", (2, 16, "w", "k"))
+@pytest.mark.parametrize("c", (2, 16, "w"))
 def test_team_unpacked_slots(W, oracle, c):
     el = W.gen_er(3000, 6.0, 7)
     el.w = (np.random.default_rng(7).integers(1, 1_100_000, len(el))).astype(np.float64)
