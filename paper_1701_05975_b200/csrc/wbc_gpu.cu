@@ -141,7 +141,7 @@ struct wbc_gpu_graph {
   LaunchShape shape_cache{};
   int ws_want = -1, ws_slots_cached = 0;
   int ws_shape_key = -1;      // launch shape the workspace was carved for
-  int tune_fill = 0;          // opt-in: measured slower (R-MAT-24 C=16: 31.3 vs 32.5 GTEPS)
+  int tune_fill = -1;         // -1 auto (the fill teams' distances fit the L2 budget), 0 off, 1 on
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   unsigned long long* d_counter = nullptr;
@@ -239,6 +239,10 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g);
 
 LaunchShape pick_shape(wbc_gpu_graph* g);
 
+// In-flight distance arrays of the team kernel's resident sources, summed:
+// kept near the 126 MB L2 (launch-shape policy below).
+constexpr uint64_t kTeamL2Budget = 128ULL << 20;
+
 // bc_flat_kernel: CTA size (two CTAs per SM: its phases are latency-bound)
 constexpr int kFlatT = 1024;  // default; set_param("flat_threads", 256 | 512 | 1024)
 
@@ -300,14 +304,15 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   // cluster whose in-flight distance arrays stay near L2 size: one CTA per
   // source while 148 of them fit in 64 MB (BA-65536: 27.5 vs 18.0 GTEPS for
   // the per-CTA kernel), else the smallest C in {2,4,8,16} with
-  // (148/C) * 4n <= 256 MB (R-MAT-20: C=2, 43 GTEPS; R-MAT-24: C=16, 32.8
-  // vs 21.8 at C=2).  Measured on B200, DESIGN.md §4.
+  // (148/C) * 4n <= kTeamL2Budget (R-MAT-20: C=4 with 2-CTA fill teams on
+  // the SMs 4-CTA clusters strand, 48.6 vs 46.3 GTEPS at C=2; R-MAT-24: C=16,
+  // 34.0 vs 31.9 at C=8 and 21.8 at C=2).  Measured on B200, DESIGN.md §4.
   if (g->tune_cluster < 0 && !tiny && g->skewed) {
     const uint64_t per = n * 4;
     int c = 1;
     if (per * static_cast<uint64_t>(g->sm_count) > (64ULL << 20)) {
       c = 2;
-      while (c < 16 && per * static_cast<uint64_t>(g->sm_count / c) > (256ULL << 20)) c *= 2;
+      while (c < 16 && per * static_cast<uint64_t>(g->sm_count / c) > kTeamL2Budget) c *= 2;
     }
     s.cluster = c;
     s.threads = 1024;
@@ -528,9 +533,13 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
   // CTAs leave 36 of 148 SMs idle): a concurrent launch of 2-CTA clusters
   // fills them, sharing the source counter.
   int fill = 0;
-  if (team && shape.cluster >= 4 && g->tune_fill && want > slots) {
+  if (team && shape.cluster >= 4 && g->tune_fill != 0 && want > slots) {
     fill = std::max(0, (g->sm_count - slots * shape.cluster) / 2);
     fill = std::min<int>(fill, want - slots);
+    // auto: only while every in-flight distance array still fits the L2
+    // budget (R-MAT-20 C=4: 33 + 8 teams x 2.6 MB, 48.6 vs 44.9 GTEPS without
+    // the fill; R-MAT-24 C=8: 27.2 vs 31.9 -- the extra teams thrash L2)
+    if (g->tune_fill < 0 && uint64_t(slots + fill) * g->n * 4 > kTeamL2Budget) fill = 0;
     if (fill > 0)
       for (const bool prof : {false, true})
         WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(2, shape.threads, g->packed, prof)),
@@ -696,7 +705,7 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
   WBC_CUDA_TRY(cudaGetLastError());
   g->stats[0] = slots;
   g->stats[1] = shape.threads * std::max(1, shape.cluster);
-  g->last_kernel = shape.flat ? std::string("bc_flat_kernel")
+  g->last_kernel = shape.flat ? "bc_flat_kernel<" + std::to_string(shape.threads) + "," + std::to_string(g->flat_ke) + ">"
                   : shape.cluster > 0 ? "bc_team_kernel<" + std::to_string(shape.threads) + "," +
                                             std::to_string(shape.cluster) + ">"
                                       : "bc_sources_kernel<" + std::to_string(shape.threads) + ">";

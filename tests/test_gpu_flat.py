@@ -40,7 +40,7 @@ def test_flat_matches_oracle(W, oracle, delta):
         try:
             src = None if g.n <= 64 else W.sample_sources(g.n, 48, 3)
             check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
-            assert gg.last_kernel() == "bc_flat_kernel", name
+            assert gg.last_kernel().startswith("bc_flat_kernel"), name
             assert gg.last_run_stats()["flat_fallback_sources"] == 0, name
         finally:
             gg.close()
@@ -65,7 +65,7 @@ def test_flat_long_distances(W, oracle):
         gg = flat_graph(W, g)
         try:
             check_graph(W, oracle, g, edge=True, gg=gg)
-            assert gg.last_kernel() == "bc_flat_kernel"
+            assert gg.last_kernel().startswith("bc_flat_kernel")
             assert gg.last_run_stats()["flat_fallback_sources"] == 0
         finally:
             gg.close()
@@ -80,7 +80,7 @@ def test_flat_auto_grid512_vs_eq4_oracle(W, oracle):
     gg = W.GpuGraph(g)
     try:
         check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
-        assert gg.last_kernel() == "bc_flat_kernel"
+        assert gg.last_kernel().startswith("bc_flat_kernel")
         assert gg.last_run_stats()["flat_fallback_sources"] == 0
     finally:
         gg.close()
@@ -92,7 +92,7 @@ def test_flat_falls_back_when_ineligible(W, oracle):
     gg = flat_graph(W, g)
     try:
         check_graph(W, oracle, g, edge=True, gg=gg)
-        assert gg.last_kernel() != "bc_flat_kernel"
+        assert not gg.last_kernel().startswith("bc_flat_kernel")
     finally:
         gg.close()
 
@@ -135,7 +135,7 @@ def test_flat_graph_strict_merge_and_dumps_use_teams(W, ref, oracle):
         assert np.array_equal(d["dist"], o["dist"]) and np.array_equal(d["sigma"], o["sigma"])
         assert d["depth"] == o["depth"]
         r2 = gg.bc(W.EngineOptions(sources=src))
-        assert gg.last_kernel() == "bc_flat_kernel"
+        assert gg.last_kernel().startswith("bc_flat_kernel")
         assert np.abs(r2.node_bc - r.node_bc).max() <= 1e-9 * max(1.0, np.abs(r.node_bc).max())
     finally:
         gg.close()
@@ -154,13 +154,13 @@ def test_flat_refuses_asymmetric_rows(W):
     gg = flat_graph(W, g)
     try:
         gg.bc(W.EngineOptions())
-        assert gg.last_kernel() != "bc_flat_kernel"
+        assert not gg.last_kernel().startswith("bc_flat_kernel")
     finally:
         gg.close()
     ok = W.build_csr(W.assign_weights(W.gen_grid(5, 5), 1, 9, 1))
     gg = flat_graph(W, ok)
     try:
         gg.bc(W.EngineOptions())
-        assert gg.last_kernel() == "bc_flat_kernel"
+        assert gg.last_kernel().startswith("bc_flat_kernel")
     finally:
         gg.close()

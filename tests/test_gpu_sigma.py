@@ -35,6 +35,6 @@ def test_sigma_overflow_flagged(W, shape):
             assert gg.last_run_stats()["sigma_overflow"] is big, (shape, k)
             assert r.sigma_exact is (not big)
             if shape == "flat":
-                assert gg.last_kernel() == "bc_flat_kernel"
+                assert gg.last_kernel().startswith("bc_flat_kernel")
         finally:
             gg.close()

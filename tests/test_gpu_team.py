@@ -155,3 +155,34 @@ def test_one_warp_team_large_distances(W, oracle):
     gg = team_graph(W, g, "w")
     check_graph(W, oracle, g, gg=gg, sources=[0, 5, 99], edge=True)
     gg.close()
+
+
+@pytest.mark.parametrize("c", (4, 8))
+def test_team_fill_clusters(W, oracle, c):
+    """C >= 4 clusters plus the concurrent 2-CTA fill launch on the SMs they
+    strand (both share the source counter): parity on a sampled R-MAT, and
+    the launch count shows the fill ran."""
+    el = W.assign_weights(W.gen_kronecker(14, 32.0, 5), 1, 255, 5)
+    g = W.build_csr(el)
+    src = W.sample_sources(g.n, 200, 4)
+    gg = W.GpuGraph(g)
+    try:
+        gg.set_param("cluster", c)
+        gg.set_param("fill", 1)
+        check_graph(W, oracle, g, gg=gg, sources=src, edge=True)
+        assert gg.last_run_stats()["launches"] == 3
+    finally:
+        gg.close()
+
+
+def test_rmat20_auto_shape_uses_fill():
+    """The auto launch shape of R-MAT-20: 4-CTA clusters plus
+    2-CTA fill teams (the in-flight distances stay within the L2 budget)."""
+    import paper_1701_05975_b200 as W
+    g = W.build_csr(W.assign_weights(W.gen_kronecker(20, 32.0, 1), 1, 255, 1))
+    gg = W.GpuGraph(g)
+    try:
+        gg.bc(W.EngineOptions(sources=W.sample_sources(g.n, 300, 1)))
+        assert gg.last_kernel() == "bc_team_kernel<1024,4>" and gg.last_run_stats()["launches"] == 3
+    finally:
+        gg.close()
