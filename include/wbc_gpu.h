@@ -135,11 +135,12 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
  * "near_width", "hot" (shared-memory distance entries; -1 auto), "l2hot"
  * (ids whose distance accesses carry an L2 evict-last hint; -1 auto),
  * "cluster" (team kernel CTAs per source; -1 auto, 0 per-CTA kernel),
- * "warp" (1: one-warp kernel for flat graphs, 2: always), "fill" (2-CTA
- * fill clusters beside C >= 4), "flat" (distance-first kernel for flat
- * graphs: -1 auto = degree <= 8 and n >= 2^18, 0 off, 1 wherever eligible),
- * "flat_delta" (its near-far window; 0 = max weight).  Unknown names return
- * WBC_E_INVALID. */
+ * "fill" (2-CTA fill clusters beside C >= 4 on the SMs they strand; -1 auto
+ * = while the in-flight distances fit the L2 budget, 0 off, 1 on),
+ * "flat" (distance-first kernel for flat graphs: -1 auto = degree <= 8 and
+ * n >= 2^18, 0 off, 1 wherever eligible), "flat_delta" (its near-far window;
+ * 0 = max weight), "flat_threads" (its CTA size: 256, 512 or 1024).  Unknown
+ * names return WBC_E_INVALID. */
 int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value);
 
 /* Work counters of subsequent runs (off by default; a few atomics per
@@ -158,8 +159,8 @@ int wbc_gpu_last_run_stats(wbc_gpu_graph* g, uint64_t* stats4);
 
 /* The last run's outcome, read from the device after synchronising it:
  * [0]=slots used, [1]=threads per team, [2]=sources that overflowed the
- * DAG-edge buffer, [3]=kernel launches, [4]=sources the distance-first
- * kernel handed to the team kernel (0 on other launch shapes),
+ * DAG-edge buffer, [3]=kernel launches, [4]=sources handed to a fallback
+ * kernel (0: since round 2 bc_flat_kernel completes every source),
  * [5]=1 when some shortest-path count sigma reached 2^53: sigma is an
  * integer-valued fp64 count (engine.cpp:73-77) that is exact only below it,
  * so BC from such a run may differ from the reference's.  Writes

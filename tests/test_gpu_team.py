@@ -186,3 +186,4 @@ def test_rmat20_auto_shape_uses_fill():
         assert gg.last_kernel() == "bc_team_kernel<1024,4>" and gg.last_run_stats()["launches"] == 3
     finally:
         gg.close()
+
