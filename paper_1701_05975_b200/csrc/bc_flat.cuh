@@ -69,9 +69,6 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #define WBC_FLAT_PREFETCH 0
 #endif
 constexpr bool kRelaxPrefetch = WBC_FLAT_PREFETCH;  // prefetch a pushed vertex's ELL row into L2
-#ifndef WBC_FLAT_B1
-#define WBC_FLAT_B1 2  // pass B1 positions per thread and step (KE = 4)
-#endif
 #ifndef WBC_FLAT_SWEEPERS
 #define WBC_FLAT_SWEEPERS 1
 #endif
@@ -93,7 +90,6 @@ struct FlatWs {
   double* pcoef;            // by position: (1 + delta) / sigma, 0 until final
   uint32_t* pinfo;          // by position: successor mask | predecessor mask << 8
   uint32_t* psucc;          // by position: KE neighbour positions (successor slots only)
-  uint32_t* ppred;          // by position: KE predecessor positions (0 elsewhere)
   uint32_t* ent;            // by position: KE sweep entries (w + minw(v)) | (d(v) - d(u)) << 16, 0 = none
                             // (two buffers, like ord_d)
   const uint32_t* ell;      // n x 2KE words: KE slots (neighbour << wbits | weight, weight 0 = empty),
@@ -370,7 +366,6 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
   double* const pcoef = w.pcoef + off;
   uint32_t* const pinfo = w.pinfo + off;
   uint32_t* const psucc = w.psucc + off * KE;
-  uint32_t* const ppred = w.ppred + off * KE;
   uint32_t* const hist = smem;
   const uint32_t wbits = g.wbits, wmask = g.wmask;
   // the sweep inputs are double-buffered per sweeper: buffer (j, parity)
@@ -657,22 +652,24 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       atomicAdd(p.prof + kProfRefills, static_cast<unsigned long long>(windows));
     }
 
-    // ---- B1. per position, no dependencies (thread-parallel, kB1 positions
-    // per thread and step in flight together): the DAG masks, successor and
-    // predecessor positions, and the sweep entries, all written coalesced;
-    // pcoef cleared for pass C.
-    constexpr int kB1 = KE == 4 ? WBC_FLAT_B1 : 1;
-    for (uint32_t q0 = gt; q0 < reached; q0 += TG * kB1) {
-      uint32_t v[kB1], dv[kB1], r[kB1][KE], kk[kB1][KE];
-      uint2 nb[kB1][KE];
+    // ---- B. sigma in distance order, a block of kBlk positions at a time.
+    // Predecessors in earlier blocks are final (global psig); those inside
+    // the block are resolved by barrier rounds over the block's shared-memory
+    // copy (0 = not yet final: sigma >= 1).  The same pass writes per
+    // position the successor mask and positions, the sweep entries, and
+    // clears pcoef for pass C -- all coalesced.
+    for (uint32_t a = 0; a < reached; a += kBlk) {
+      uint32_t v[kU], dv[kU], r[kU][KE], kk[kU][KE], sp[kU][KE], pend[kU];
+      uint2 nb[kU][KE];
+      double sg[kU];
 #pragma unroll
-      for (int j = 0; j < kB1; ++j) {
-        const uint32_t q = q0 + j * TG;
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + gt + j * TG;
         v[j] = q < reached ? __ldcg(order + q) : 0u;
         dv[j] = q < reached ? __ldcg(ord_d + q) : kInfDist;
       }
 #pragma unroll
-      for (int j = 0; j < kB1; ++j) {
+      for (int j = 0; j < kU; ++j) {
         if (dv[j] != kInfDist) {
           ell_row<KE>(w, v[j], r[j]);
           ell_keys<KE>(w, v[j], kk[j]);
@@ -682,79 +679,49 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         }
       }
 #pragma unroll
-      for (int j = 0; j < kB1; ++j)
+      for (int j = 0; j < kU; ++j)
 #pragma unroll
         for (int x = 0; x < KE; ++x)
           nb[j][x] = (r[j][x] & wmask) ? __ldcg(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
 #pragma unroll
-      for (int j = 0; j < kB1; ++j) {
-        const uint32_t q = q0 + j * TG;
-        if (q >= reached) continue;
-        uint32_t pm = 0, sm = 0, e[KE], sp[KE], pp[KE];
+      for (int j = 0; j < kU; ++j) {
+        const uint32_t q = a + gt + j * TG;
+        pend[j] = 0;
+        sg[j] = 0.0;
+        uint32_t pm = 0, sm = 0, e[KE];
 #pragma unroll
         for (int x = 0; x < KE; ++x) {
           const uint32_t wt = r[j][x] & wmask, d = nb[j][x].x;
           e[x] = 0;
-          sp[x] = nb[j][x].y;
-          pp[x] = 0;
+          sp[j][x] = nb[j][x].y;
           if (!wt || d == kInfDist) continue;  // padding (a reached vertex's neighbours are reached)
-          if (d + wt == dv[j]) {
-            pm |= 1u << x;
-            pp[x] = sp[x];
-          }
+          if (d + wt == dv[j]) pm |= 1u << x;
           if (dv[j] + wt == d) sm |= 1u << x;
           if (d > dv[j]) e[x] = kk[j][x] | (d - dv[j]) << 16;
         }
+        if (q >= reached) continue;
         __stcg(pcoef + q, 0.0);
         __stcg(pinfo + q, sm | pm << 8);
         uint4* const so = reinterpret_cast<uint4*>(psucc + static_cast<uint64_t>(q) * KE);
-        uint4* const po = reinterpret_cast<uint4*>(ppred + static_cast<uint64_t>(q) * KE);
         uint4* const eo = reinterpret_cast<uint4*>(ent + static_cast<uint64_t>(q) * KE);
 #pragma unroll
         for (int x = 0; x < KE / 4; ++x) {
-          __stcg(so + x, make_uint4(sp[4 * x], sp[4 * x + 1], sp[4 * x + 2], sp[4 * x + 3]));
-          __stcg(po + x, make_uint4(pp[4 * x], pp[4 * x + 1], pp[4 * x + 2], pp[4 * x + 3]));
+          __stcg(so + x, make_uint4(sp[j][4 * x], sp[j][4 * x + 1], sp[j][4 * x + 2], sp[j][4 * x + 3]));
           __stcg(eo + x, make_uint4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]));
         }
-      }
-    }
-    gsync();
-
-    // ---- B2. sigma in distance order, a block of kBlk positions at a time:
-    // predecessors in earlier blocks are final (global psig, a few thousand
-    // positions back: L2); those inside the block resolve by barrier rounds
-    // over the block's shared-memory copy (0 = not yet final: sigma >= 1).
-    for (uint32_t a = 0; a < reached; a += kBlk) {
-      uint32_t pm[kU], sp[kU][KE], pend[kU];
-      double sg[kU];
+        if (q == 0) {
+          sg[j] = 1.0;  // the source (the only vertex at distance 0)
+        } else {
 #pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        const uint32_t q = a + gt + j * TG;
-        pm[j] = q < reached ? (__ldcg(pinfo + q) >> 8) & 0xFFu : 0u;
-        const uint4* po = reinterpret_cast<const uint4*>(ppred + static_cast<uint64_t>(q) * KE);
-#pragma unroll
-        for (int x = 0; x < KE / 4; ++x) {
-          const uint4 t4 = pm[j] ? __ldcg(po + x) : make_uint4(0, 0, 0, 0);
-          sp[j][4 * x] = t4.x;
-          sp[j][4 * x + 1] = t4.y;
-          sp[j][4 * x + 2] = t4.z;
-          sp[j][4 * x + 3] = t4.w;
+          for (int x = 0; x < KE; ++x)
+            if (pm >> x & 1u) {
+              if (sp[j][x] < a)
+                sg[j] += __ldcg(psig + sp[j][x]);
+              else
+                pend[j] |= 1u << x;
+            }
         }
-      }
-#pragma unroll
-      for (int j = 0; j < kU; ++j) {
-        const uint32_t q = a + gt + j * TG;
-        pend[j] = 0;
-        sg[j] = q == 0 ? 1.0 : 0.0;  // the source (the only vertex at distance 0)
-#pragma unroll
-        for (int x = 0; x < KE; ++x)
-          if (pm[j] >> x & 1u) {
-            if (sp[j][x] < a)
-              sg[j] += __ldcg(psig + sp[j][x]);
-            else
-              pend[j] |= 1u << x;
-          }
-        if (q < reached) s_blk[q - a] = pend[j] ? 0.0 : sg[j];
+        s_blk[q - a] = pend[j] ? 0.0 : sg[j];
       }
       for (;;) {
         uint32_t any = 0;

@@ -378,7 +378,7 @@ uint64_t flat_ns(const wbc_gpu_graph* g) { return round_up(uint64_t{g->n} + 2, w
 uint64_t ws_flat_per_slot(const wbc_gpu_graph* g) {
   const uint64_t ke = static_cast<uint64_t>(std::max(4, g->flat_ke));
   const uint64_t bufs = 2 * wbc_dev::kSweepers;  // sweep inputs: two buffers per sweeper warp
-  return flat_ns(g) * (8 + 4 + bufs * 4 + 4 + 16 + 8 + 8 + 4 + 2 * 4 * ke + bufs * 4 * ke);
+  return flat_ns(g) * (8 + 4 + bufs * 4 + 4 + 16 + 8 + 8 + 4 + 4 * ke + bufs * 4 * ke);
 }
 
 void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
@@ -394,7 +394,6 @@ void carve_flat(wbc_gpu_graph* g, char* p, uint64_t slots) {
   w.psig = reinterpret_cast<double*>(carve(ns * 8));
   w.pcoef = reinterpret_cast<double*>(carve(ns * 8));
   w.psucc = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
-  w.ppred = reinterpret_cast<uint32_t*>(carve(ns * 4 * ke));
   const uint64_t bufs = 2 * wbc_dev::kSweepers;
   w.ent = reinterpret_cast<uint32_t*>(carve(bufs * ns * 4 * ke));  // two buffers per sweeper
   w.order = reinterpret_cast<uint32_t*>(carve(ns * 4));

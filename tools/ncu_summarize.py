@@ -61,7 +61,7 @@ def main():
     wr = float(m["dram__bytes_write.sum"][0].replace(",", ""))
     scale = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
     tot = rd * scale[m["dram__bytes_read.sum"][1]] + wr * scale[m["dram__bytes_write.sum"][1]]
-    print(f"\nDRAM traffic per source: **{tot / a.sources / 1e9:.3f} GB** (read+write)\n")
+    print(f"\nDRAM traffic per source: **{tot / a.sources / 1e9:.4g} GB** (read+write)\n")
     print("Top source lines by warp-stall samples (line '' = inline PTX loads without line info):\n")
     print("| line | stall % | L2 sectors % | source |\n|---|---|---|---|")
     for k, s, l2, src in lines(a.rep, a.top):

@@ -1,5 +1,4 @@
 # flat kernel checks (one gpurun call)
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_flat.py tests/test_gpu_sigma.py -x -q > gpurun_out/flat_tests.log 2>&1; echo tests rc=$?; tail -4 gpurun_out/flat_tests.log
-python tools/sweep_data.py /tmp/sweep 2048 >/dev/null && ./tools/_bin/sweep_bench /tmp/sweep 148 | tail -2
-bash tools/r2_ab.sh "--graph grid2048 --k 1024 --reps 2 --prof" default sw2
+bash tools/r2_ab.sh "--graph grid2048 --k 1024 --reps 2 --prof" default b13 b14
