@@ -27,7 +27,7 @@ extern "C" {
  * engine.cpp:110-114,354,373-374) and everything else to std::runtime_error. */
 #define WBC_OK 0
 #define WBC_E_INVALID (-1)     /* bad argument: source out of range, bad graph arrays */
-#define WBC_E_UNSUPPORTED (-2) /* weights not positive integers, distance bound >= 2^32 */
+#define WBC_E_UNSUPPORTED (-2) /* weights not positive integers or dyadic fractions, distance bound >= 2^32 */
 #define WBC_E_CUDA (-3)        /* CUDA runtime failure (message has cudaGetErrorString) */
 #define WBC_E_NOMEM (-4)       /* device allocation failed */
 #define WBC_E_NOT_BUILT (-5)   /* library built without a usable sm_100a device */
@@ -54,9 +54,12 @@ typedef struct wbc_gpu_graph wbc_gpu_graph;
  *   offsets[n+1], adjacency[2m], weights[2m], min_incident_weight[n]
  *   (+inf for isolated vertices), edge_id[2m] (nullable: edge BC then
  *   unavailable).  Weights must be positive integers (all reference configs
- *   use assign_weights integers, generate.cpp:121-128) and (n-1)*max_weight
- *   must stay below 2^32-1 so that distances are exact u32 (else
- *   WBC_E_UNSUPPORTED).  device < 0 selects the current CUDA device. */
+ *   use assign_weights integers, generate.cpp:121-128) or dyadic fractions
+ *   i / 2^k (k <= 20; e.g. 0.5, 2.5), which run scaled by the common 2^K:
+ *   power-of-two scaling is exact in fp64, so the reference's distances are
+ *   2^-K times exact integers.  (n-1)*max_weight (scaled) must stay below
+ *   2^32-1 so that distances are exact u32; anything else returns
+ *   WBC_E_UNSUPPORTED.  device < 0 selects the current CUDA device. */
 int wbc_gpu_graph_create(uint32_t n, uint32_t m, const uint32_t* offsets,
                          const uint32_t* adjacency, const double* weights,
                          const double* min_incident_weight, const uint32_t* edge_id,

@@ -165,6 +165,7 @@ struct wbc_gpu_graph {
   int tune_flat_threads = 0;     // bc_flat_kernel CTA size (0: kFlatT)
   uint32_t max_degree = 0, max_minw = 0;
   bool symmetric = false;
+  int scale_k = 0;             // weights scaled by 2^scale_k to integers (dumps scale distances back)
   wbc_dev::FlatWs fw{};
   int tune_cluster = -1;       // -1 auto, 0 per-CTA kernel, else team kernel with this cluster size
   bool ws_team = false;        // workspace carries the team-kernel arrays
@@ -242,6 +243,9 @@ LaunchShape pick_shape(wbc_gpu_graph* g);
 // In-flight distance arrays of the team kernel's resident sources, summed:
 // kept near the 126 MB L2 (launch-shape policy below).
 constexpr uint64_t kTeamL2Budget = 128ULL << 20;
+
+// Largest power-of-two denominator of a dyadic weight (prepare_host).
+constexpr int kMaxWeightScaleBits = 20;
 
 // bc_flat_kernel: CTA size (two CTAs per SM: its phases are latency-bound)
 constexpr int kFlatT = 1024;  // default; set_param("flat_threads", 256 | 512 | 1024)
@@ -820,6 +824,7 @@ namespace {
 struct HostCsr {
   uint32_t n = 0, m = 0, max_weight = 0, wbits = 0, near_width = 1, max_degree = 0, max_minw = 0;
   bool symmetric = false;  // every slot u->v (w) has a twin v->u (w); checked for low-degree graphs
+  int scale_k = 0;         // weights were scaled by 2^scale_k to integers
   bool packed = true, skewed = false, has_edge_id = false;
   double hot_coverage_25k = 0;
   std::vector<uint32_t> perm, inv, noff, slot32, eid, minw, ref_slot32, ref_eid;
@@ -857,30 +862,56 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
       }
   });
   if (bad_off.load() != UINT64_MAX) return set_error(WBC_E_INVALID, "offsets not monotone");
+  // Weights: positive dyadic rationals w = i / 2^k (integers k = 0, and e.g.
+  // 0.5 or 2.5), scaled by the common 2^K to integers.  Scaling by a power of
+  // two is exact in fp64, so every distance the reference computes is 2^-K
+  // times an exact integer sum (while below 2^53, which the u32 bound below
+  // implies): distances, ties, the Eq. 4 thresholds d + minw (hence
+  // depth_per_source) and sigma / delta / BC are those of the integer graph.
+  std::atomic<int> scale_k{0};
   parallel_for(slots, [&](uint64_t b, uint64_t e) {
-    uint64_t mw = 0;
+    int kk = 0;
     for (uint64_t x = b; x < e; ++x) {
       const double w = weights[x];
       if (adjacency[x] >= n) {
         atomic_min(bad_adj, x);
         break;
       }
-      if (!(w >= 1.0) || w != std::floor(w) || w > 4294967295.0) {
+      if (!(w > 0.0) || !std::isfinite(w)) {
         atomic_min(bad_w, x);
         break;
       }
-      mw = std::max<uint64_t>(mw, static_cast<uint64_t>(w));
+      int k = 0;
+      while (k <= kMaxWeightScaleBits && std::ldexp(w, k) != std::floor(std::ldexp(w, k))) ++k;
+      if (k > kMaxWeightScaleBits) {
+        atomic_min(bad_w, x);
+        break;
+      }
+      kk = std::max(kk, k);
+    }
+    int cur = scale_k.load();
+    while (kk > cur && !scale_k.compare_exchange_weak(cur, kk)) {}
+  });
+  if (bad_adj.load() < bad_w.load()) return set_error(WBC_E_INVALID, "adjacency entry out of range");
+  if (bad_w.load() != UINT64_MAX)
+    return set_error(WBC_E_UNSUPPORTED,
+                     "weights must be positive integers or dyadic fractions i / 2^k, k <= " +
+                         std::to_string(kMaxWeightScaleBits) + " (exact integer distances on the GPU); got " +
+                         std::to_string(weights[bad_w.load()]));
+  const int K = scale_k.load();
+  h.scale_k = K;
+  parallel_for(slots, [&](uint64_t b, uint64_t e) {
+    uint64_t mw = 0;
+    for (uint64_t x = b; x < e; ++x) {
+      const double w = std::ldexp(weights[x], K);
+      mw = std::max<uint64_t>(mw, w > 4294967295.0 ? UINT64_MAX : static_cast<uint64_t>(w));
     }
     uint64_t cur = maxw_a.load();
     while (mw > cur && !maxw_a.compare_exchange_weak(cur, mw)) {}
   });
-  if (bad_adj.load() < bad_w.load()) return set_error(WBC_E_INVALID, "adjacency entry out of range");
-  if (bad_w.load() != UINT64_MAX)
-    return set_error(WBC_E_UNSUPPORTED, "weights must be positive integers (exact u32 distances); got " +
-                                            std::to_string(weights[bad_w.load()]));
   const uint64_t maxw = maxw_a.load();
-  if (n > 0 && uint64_t{n} * std::max<uint64_t>(maxw, 1) >= 0xFFFFFFFFULL)
-    return set_error(WBC_E_UNSUPPORTED, "n * max_weight must stay below 2^32-1");
+  if (maxw > 0xFFFFFFFFULL || (n > 0 && uint64_t{n} * std::max<uint64_t>(maxw, 1) >= 0xFFFFFFFFULL))
+    return set_error(WBC_E_UNSUPPORTED, "n * max_weight (scaled to integers) must stay below 2^32-1");
   h.n = n;
   h.m = m;
   h.has_edge_id = edge_id != nullptr;
@@ -924,8 +955,8 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
     if (std::isinf(x) || offsets[v + 1] == offsets[v]) {
       h.minw[i] = wbc_dev::kInfDist;
     } else {
-      h.minw[i] = static_cast<uint32_t>(x);
-      sum_minw += x;
+      h.minw[i] = static_cast<uint32_t>(std::ldexp(x, K));
+      sum_minw += std::ldexp(x, K);
       ++cnt_minw;
     }
   }
@@ -939,7 +970,7 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
       for (uint32_t s = offsets[v]; s < offsets[v + 1]; ++s) row.emplace_back(inv[adjacency[s]], s);
       uint32_t o = noff[i];
       for (const auto& [u, s] : row) {  // caller's order (strict merge)
-        const uint32_t w = static_cast<uint32_t>(weights[s]);
+        const uint32_t w = static_cast<uint32_t>(std::ldexp(weights[s], K));
         if (packed)
           h.ref_slot32[o] = (u << wbits) | w;
         else
@@ -950,7 +981,7 @@ int prepare_host(uint32_t n, uint32_t m, const uint32_t* offsets, const uint32_t
       std::sort(row.begin(), row.end());
       o = noff[i];
       for (const auto& [u, s] : row) {
-        const uint32_t w = static_cast<uint32_t>(weights[s]);
+        const uint32_t w = static_cast<uint32_t>(std::ldexp(weights[s], K));
         if (packed)
           h.slot32[o] = (u << wbits) | w;
         else
@@ -1056,6 +1087,7 @@ int upload_graph(const HostCsr& h, int device, wbc_gpu_graph** out) {
   g->max_degree = h.max_degree;
   g->max_minw = h.max_minw;
   g->symmetric = h.symmetric;
+  g->scale_k = h.scale_k;
   const bool packed = h.packed;
   g->d_offsets = dev_alloc<uint32_t>(uint64_t{n} + 1, err);
   if (err == cudaSuccess) g->d_minw = dev_alloc<uint32_t>(n, err);
@@ -1353,7 +1385,7 @@ int wbc_gpu_sssp_dump(wbc_gpu_graph* g, uint32_t source, double* dist, double* s
     if (dist)
       for (uint64_t i = 0; i < n; ++i) {
         const uint32_t d = du[i];
-        dist[g->perm[i]] = d == wbc_dev::kInfDist ? HUGE_VAL : static_cast<double>(d);
+        dist[g->perm[i]] = d == wbc_dev::kInfDist ? HUGE_VAL : std::ldexp(static_cast<double>(d), -g->scale_k);
       }
     if (sigma) {
       WBC_CUDA_TRY(cudaMemcpy(tmp.data(), st.sigma, n * 8, cudaMemcpyDeviceToHost));

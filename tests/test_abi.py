@@ -70,12 +70,18 @@ def test_c_abi_error_paths_without_gpu():
     import numpy as np
     off = np.array([0, 1, 2], np.uint32)
     adj = np.array([1, 0], np.uint32)
-    w = np.array([1.5, 1.5])                      # fractional weight -> unsupported
-    mw = np.array([1.5, 1.5])
+    w = np.array([0.1, 0.1])                      # not a dyadic fraction i / 2^k -> unsupported
+    mw = np.array([0.1, 0.1])
     rc = lib.wbc_gpu_graph_create(2, 1, off.ctypes.data, adj.ctypes.data, w.ctypes.data, mw.ctypes.data, None,
                                   -1, ctypes.byref(h))
     assert rc == _lib.WBC_E_UNSUPPORTED
-    assert "integer" in _lib.last_error()
+    assert "dyadic" in _lib.last_error()
+    for bad_w in (0.0, -1.0, float("inf")):       # weights must be positive and finite
+        w2 = np.array([bad_w, bad_w])
+        rc = lib.wbc_gpu_graph_create(2, 1, off.ctypes.data, adj.ctypes.data, w2.ctypes.data, w2.ctypes.data,
+                                      None, -1, ctypes.byref(h))
+        assert rc == _lib.WBC_E_UNSUPPORTED
+    w = np.array([1.5, 1.5])
     bad = np.array([0, 1, 3], np.uint32)          # offsets[n] != 2m
     rc = lib.wbc_gpu_graph_create(2, 1, bad.ctypes.data, adj.ctypes.data, w.ctypes.data, mw.ctypes.data, None,
                                   -1, ctypes.byref(h))

@@ -264,3 +264,40 @@ def test_ba_sampled_vs_oracle(W, oracle):
     g = W.build_csr(el)
     src = W.sample_sources(g.n, 64, 1)
     check_graph(W, oracle, g, sources=src, edge=True)
+
+
+def test_dyadic_fractional_weights(W, oracle):
+    """Weights i / 2^k (0.5, 2.5, 1.25, ...; the SPEC's own `0 1 2.5` example)
+    run as integers scaled by 2^K: fp64 distances are exact multiples of
+    2^-K, so dist, sigma, depth and BC equal the reference's."""
+    rng = np.random.default_rng(5)
+    el = W.gen_er(300, 6.0, 5)
+    el.w = rng.choice([0.5, 1.25, 2.5, 3.0, 0.75, 7.125], len(el)).astype(np.float64)
+    g = W.build_csr(el)
+    check_graph(W, oracle, g, edge=True)
+    src = W.sample_sources(g.n, 12, 2)
+    check_sources_dump(W, oracle, g, src)
+    for shape in ({"cluster": 1}, {"cluster": 2}, {"cluster": 1, "threads": 32}, {"flat": 1}):
+        gg = W.GpuGraph(g)
+        try:
+            for k, v in shape.items():
+                gg.set_param(k, v)
+            check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
+        finally:
+            gg.close()
+    grid = W.build_csr(W.EdgeList(*[np.asarray(a) for a in (W.gen_grid(20, 20).u, W.gen_grid(20, 20).v)],
+                                  rng.choice([0.5, 1.5, 2.25], 2 * 20 * 19).astype(np.float64)))
+    gg = W.GpuGraph(grid)
+    try:
+        gg.set_param("flat", 1)
+        check_graph(W, oracle, grid, edge=True, gg=gg)
+        assert gg.last_kernel().startswith("bc_flat_kernel")
+    finally:
+        gg.close()
+
+
+def test_non_dyadic_weights_are_refused(W):
+    el = W.gen_er(50, 4.0, 3)
+    el.w = np.full(len(el), 0.1)
+    with pytest.raises(RuntimeError, match="dyadic"):
+        W.GpuGraph(W.build_csr(el))

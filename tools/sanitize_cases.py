@@ -21,11 +21,14 @@ cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("team C=2", kron, {"cluster": 2}),
          ("team C=4", kron, {"cluster": 4}),
          ("one-warp team", grid, {"cluster": 1, "threads": 32}),
-         ("flat kernel", grid, {"flat": 1}),
-         ("flat kernel + team fallback", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
+         ("team C=4 + 2-CTA fill", kron, {"cluster": 4, "fill": 1}),
+         ("flat kernel, 1024 threads", grid, {"flat": 1, "slots": 3}),
+         ("flat kernel, 256 threads", grid, {"flat": 1, "flat_threads": 256, "slots": 2}),
+         ("flat kernel, long distances", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
+         ("flat kernel, unit weights", W.build_csr(W.assign_weights(W.gen_grid(12, 10), 1, 1, 3)), {"flat": 1}),
          ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8})]
 for name, g, params in cases:
-    src = W.sample_sources(g.n, 6, 1)
+    src = W.sample_sources(g.n, 12 if params.get("flat") else 6, 1)  # flat: more sources than CTAs cycle the sweep buffers
     gg = W.GpuGraph(g, 0)
     strict = params.pop("_strict", 0)
     for k, v in params.items():
