@@ -353,7 +353,6 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
   __shared__ uint32_t s_warp[T / 32];
   __shared__ double s_blk[kBlk];             // the block's sigma (B) / coef (C); 0 = not final
   __shared__ uint32_t s_sw[kSW][2][3];       // per sweeper and buffer: reached, source, exit
-  volatile double* const s_blk_v = s_blk;
   extern __shared__ uint32_t smem[];         // hist | buckets | sweep ring
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
@@ -728,20 +727,27 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
         for (int j = 0; j < kU; ++j) any |= pend[j];
         if (!gsync_or(any)) break;
+        // a round: read the values final so far, then (after a barrier) publish
+        // the ones this round completed -- reads and writes never overlap
+        uint32_t fin = 0;
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
           if (!pend[j]) continue;
 #pragma unroll
           for (int x = 0; x < KE; ++x)
             if (pend[j] >> x & 1u) {
-              const double y = s_blk_v[sp[j][x] - a];
+              const double y = s_blk[sp[j][x] - a];
               if (y != 0.0) {
                 sg[j] += y;
                 pend[j] &= ~(1u << x);
               }
             }
-          if (!pend[j]) s_blk_v[gt + j * TG] = sg[j];
+          if (!pend[j]) fin |= 1u << j;
         }
+        gsync();
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+          if (fin >> j & 1u) s_blk[gt + j * TG] = sg[j];
       }
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
@@ -811,13 +817,14 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
         for (int j = 0; j < kU; ++j) any |= pend[j];
         if (!gsync_or(any)) break;
+        uint32_t fin = 0;  // a round: reads, barrier, then this round's completions
 #pragma unroll
         for (int j = 0; j < kU; ++j) {
           if (!pend[j]) continue;
 #pragma unroll
           for (int x = 0; x < KE; ++x)
             if (pend[j] >> x & 1u) {
-              const double y = s_blk_v[sp[j][x] - a];
+              const double y = s_blk[sp[j][x] - a];
               if (y != 0.0) {
                 const double c = su[j] * y;
                 dsum[j] += c;
@@ -825,8 +832,12 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
                 pend[j] &= ~(1u << x);
               }
             }
-          if (!pend[j]) s_blk_v[bend - 1 - (gt + j * TG) - a] = (1.0 + dsum[j]) / su[j];
+          if (!pend[j]) fin |= 1u << j;
         }
+        gsync();
+#pragma unroll
+        for (int j = 0; j < kU; ++j)
+          if (fin >> j & 1u) s_blk[bend - 1 - (gt + j * TG) - a] = (1.0 + dsum[j]) / su[j];
       }
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
