@@ -24,6 +24,17 @@ elif a.graph == "er":
     el = W.assign_weights(W.gen_er(4096, 8.0, 1), 1, 64, 1)
 elif a.graph == "ba":
     el = W.assign_weights(W.gen_ba(65536, 10, 1), 1, 100, 1)
+elif a.graph.startswith("mortongrid"):  # the same grid (same weights), vertex ids in Morton order
+    s = int(a.graph[10:]); el = W.assign_weights(W.gen_grid(s, s), 1, 1000, 1)
+    def morton(i):
+        r, c = np.asarray(i) // s, np.asarray(i) % s
+        z = np.zeros_like(r)
+        for b in range(16):
+            z |= ((c >> b) & 1) << (2 * b) | ((r >> b) & 1) << (2 * b + 1)
+        return z
+    mu, mv = morton(el.u.astype(np.int64)), morton(el.v.astype(np.int64))
+    o = np.argsort(np.minimum(mu, mv) * 4 + (mu > mv), kind="stable")  # first appearance follows Morton order
+    el = W.EdgeList(mu[o].astype(np.uint64), mv[o].astype(np.uint64), el.w[o])
 elif a.graph.startswith("grid"):
     s = int(a.graph[4:]); el = W.assign_weights(W.gen_grid(s, s), 1, 1000, 1)
 g = W.build_csr(el)
