@@ -139,7 +139,8 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
  * (ids whose distance accesses carry an L2 evict-last hint; -1 auto),
  * "cluster" (team kernel CTAs per source; -1 auto, 0 per-CTA kernel),
  * "fill" (2-CTA fill clusters beside C >= 4 on the SMs they strand; -1 auto
- * = while the in-flight distances fit the L2 budget, 0 off, 1 on),
+ * = while the in-flight distances fit the L2 budget, 0 off, 1 on, k > 1: at
+ * most k - 1 fill teams),
  * "flat" (distance-first kernel for flat graphs: -1 auto = degree <= 8 and
  * n >= 2^18, 0 off, 1 wherever eligible), "flat_delta" (its near-far window;
  * 0 = max weight), "flat_threads" (its CTA size: 256, 512 or 1024).  Unknown

@@ -544,6 +544,7 @@ int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* 
     // budget (R-MAT-20 C=4: 33 + 8 teams x 2.6 MB, 48.6 vs 44.9 GTEPS without
     // the fill; R-MAT-24 C=8: 27.2 vs 31.9 -- the extra teams thrash L2)
     if (g->tune_fill < 0 && uint64_t(slots + fill) * g->n * 4 > kTeamL2Budget) fill = 0;
+    if (g->tune_fill > 1) fill = std::min(fill, g->tune_fill - 1);  // tests / experiments: at most fill - 1 teams
     if (fill > 0)
       for (const bool prof : {false, true})
         WBC_CUDA_TRY(cudaFuncSetAttribute(reinterpret_cast<const void*>(pick_team(2, shape.threads, g->packed, prof)),
