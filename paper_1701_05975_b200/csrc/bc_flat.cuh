@@ -182,6 +182,18 @@ __device__ __forceinline__ void ell_keys(const FlatWs& w, uint32_t v, uint32_t (
   }
 }
 __device__ __forceinline__ uint32_t* dist_of(uint2* dp, uint32_t v) { return reinterpret_cast<uint32_t*>(dp + v); }
+// The whole KE = 4 record (slots and keys, 32 bytes) in one 256-bit load.
+__device__ __forceinline__ void ell_rec4(const FlatWs& w, uint32_t v, uint32_t (&r)[4], uint32_t (&k)[4]) {
+  const uint32_t* p = w.ell + static_cast<uint64_t>(v) * 8;
+  uint32_t k01, k23, z0, z1;
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(k01), "=r"(k23), "=r"(z0), "=r"(z1)
+      : "l"(p));
+  k[0] = k01 & 0xFFFFu;
+  k[1] = k01 >> 16;
+  k[2] = k23 & 0xFFFFu;
+  k[3] = k23 >> 16;
+}
 
 // The Eq. 4 threshold sweep of one source, run by one warp: ord_d / ent are
 // the source's sorted distances and sweep entries (reached positions);
@@ -670,8 +682,12 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         if (dv[j] != kInfDist) {
-          ell_row<KE>(w, v[j], r[j]);
-          ell_keys<KE>(w, v[j], kk[j]);
+          if constexpr (KE == 4) {
+            ell_rec4(w, v[j], r[j], kk[j]);
+          } else {
+            ell_row<KE>(w, v[j], r[j]);
+            ell_keys<KE>(w, v[j], kk[j]);
+          }
         } else {
 #pragma unroll
           for (int x = 0; x < KE; ++x) r[j][x] = kk[j][x] = 0;
