@@ -10,12 +10,19 @@ strong scaling).  Other configs: --workload er4096 | ba65536 | grid2048 | rmat20
   python bench.py [--gpus N --steps K --warmup W]      # our GPU arm
   python bench.py --impl reference                      # the reference's CPU bc_parallel
 
+--gpus N without a launcher re-runs this command under torch.distributed.run
+with N ranks (one NCCL rank per GPU; fails loudly with fewer GPUs); rank 0
+builds the graph once and the others map its arrays.
+
 The JSON line carries: value (device-timed, inputs resident), e2e (through the
 host-buffer C ABI wbc_gpu_bc, H2D sources + D2H results inside the timing),
 roofline of the BC kernel (algorithmic bytes 72m+88n per source, SURVEY.md §8d,
-over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs),
-cpu_baseline (the compiled reference on this host's cores, bounded sample),
-clocks sampled during the timed region and gpu_launches.
+over its CUDA-event launch time, against MEASURED_PEAKS.json hbm_gbs, with the
+ncu DRAM bytes of the same kernel shape from profiles/ncu_traffic.json),
+cpu_baseline (the compiled reference on this host's cores, bounded samples:
+brandes_sequential x cores and on one core, bc_parallel with its best strategy),
+score_gate (the GPU BC of those samples vs the reference's, 1e-9 relative, and
+depth_per_source exact), clocks sampled during the timed region and gpu_launches.
 """
 from __future__ import annotations
 
