@@ -514,7 +514,9 @@ def main():
 
     built = shared_graph(wl, rank, world, barrier)
     g, src_all, t_build = built[:3]
+    t_rep = time.perf_counter()
     gg = W.GpuGraph(g, device=dev)
+    t_rep = time.perf_counter() - t_rep
     if world > 1:
         barrier()  # every rank holds its replica: the shared arrays can go
         if rank == 0:
@@ -621,7 +623,7 @@ def main():
                                 collective="none" if world == 1 else f"one {args.dist_backend} all_reduce of the partial BC",
                                 nccl=nccl,
                                 l2="inputs exceed L2 (CSR replica + per-source workspaces >> 126 MB), no flush",
-                                graph_build_s=round(t_build, 2)),
+                                graph_build_s=round(t_build, 2), replica_build_s=round(t_rep, 2)),
                     e2e=dict(value=round(e2e_value, 3), unit="GTEPS", h2d_bytes_per_step=int(h2d),
                              d2h_bytes_per_step=int(d2h), api="wbc_gpu_bc (host buffers)"),
                     roofline=roofline, clocks=clk, gpu_launches=int(launches),
