@@ -42,7 +42,10 @@ namespace wbc_dev {
 namespace cg = cooperative_groups;
 
 constexpr uint32_t kInfDist = 0xFFFFFFFFu;
-constexpr int kUnroll = 2;  // 32-edge groups per warp step in relax (R-MAT-20: 1: 38.2, 2: 44.8, 3: 44.4, 4: 43.9, 6: 32.3, 8: 17.3 GTEPS)
+#ifndef WBC_TEAM_UNROLL
+#define WBC_TEAM_UNROLL 2
+#endif
+constexpr int kUnroll = WBC_TEAM_UNROLL;  // 32-edge groups per warp step in relax (R-MAT-20 at C=2: 1: 38.2, 2: 44.8, 3: 44.4, 4: 43.9, 6: 32.3, 8: 17.3 GTEPS)
 
 // ---- L2 residency hints.  The CSR slot stream (read once per source, 4 B
 // per slot, far larger than L2) is marked evict-first and skips L1; the

@@ -130,8 +130,13 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
 
 // Per-warp compaction queues of the two-pass relax (dynamic shared memory):
 // 5 arrays of kTeamQ u32 per warp; a warp holds < 32 entries between drains
-// and adds at most 32 * kUnroll per step.
-constexpr uint32_t kTeamQ = 32 * kUnroll + 32;
+// and adds at most 32 * team_unroll per step.
+// Relax groups per warp step: 3 for clusters (R-MAT-20 at C = 4: 49.7 vs 48.6
+// GTEPS at 2, 48.7 at 4; R-MAT-24: 35.3 vs 35.0), 2 for single-CTA teams
+// (BA-65536: 31.7 vs 31.5 at 3).
+template <int T, int C>
+constexpr int team_unroll() { return (C >= 2 && T >= 1024) ? 3 : kUnroll; }
+constexpr uint32_t kTeamQ = 32 * 3 + 32;
 __host__ __device__ constexpr size_t team_q_bytes(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
 template <int T>
 constexpr size_t team_sh_bytes() { return (sizeof(TeamShared<T>) + 15) / 16 * 16; }
@@ -379,26 +384,27 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
                 }
                 pq_n -= m;
               };
-              // Pass 1: stream kUnroll groups of 32 edges; software-pipelined:
+              constexpr int kTU = team_unroll<T, C>();
+              // Pass 1: stream kTU groups of 32 edges; software-pipelined:
               // the next step's slot words are in flight while this step's
               // distance gathers resolve.  Only lanes that need more work are
               // kept (compacted into the warp's queues).
               // Slot words stay packed until used (PACKED: one register).
               using Word = typename std::conditional<PACKED, uint32_t, uint2>::type;
               constexpr Word kNoWord = Word{};
-              int jj[kUnroll];
-              Word xw[kUnroll];
+              int jj[kTU];
+              Word xw[kTU];
               auto fetch = [&](uint32_t e0) {
-                uint32_t slot[kUnroll];
+                uint32_t slot[kTU];
 #pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
+                for (int k = 0; k < kTU; ++k) {
                   const uint32_t eg = e0 + 32 * k;
                   jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0, g.long_rows) : 0;
                   const uint32_t e = eg + lane;
                   slot[k] = e < we ? sh.rowadj[jj[k]] + e : 0xFFFFFFFFu;
                 }
 #pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
+                for (int k = 0; k < kTU; ++k) {
                   xw[k] = kNoWord;
                   if (slot[k] != 0xFFFFFFFFu) {
                     if constexpr (PACKED)
@@ -415,21 +421,21 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
                 if constexpr (PACKED) return x & g.wmask; else return x.y;
               };
               fetch(wb);
-              for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
+              for (uint32_t e0 = wb; e0 < we; e0 += 32 * kTU) {
                 const uint32_t cwe = we;
-                uint32_t du[kUnroll];
-                Word cx[kUnroll];
-                int cj[kUnroll];
+                uint32_t du[kTU];
+                Word cx[kTU];
+                int cj[kTU];
 #pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
+                for (int k = 0; k < kTU; ++k) {
                   const bool valid = e0 + 32 * k + lane < cwe;
                   du[k] = valid ? dist.load(nbr(xw[k])) : 0u;
                   cx[k] = xw[k];
                   cj[k] = jj[k];
                 }
-                if (e0 + 32 * kUnroll < we) fetch(e0 + 32 * kUnroll);
+                if (e0 + 32 * kTU < we) fetch(e0 + 32 * kTU);
 #pragma unroll
-                for (int k = 0; k < kUnroll; ++k) {
+                for (int k = 0; k < kTU; ++k) {
                   const uint32_t e = e0 + 32 * k + lane;
                   const bool valid = e < cwe;
                   const uint32_t dv = sh.dv[cj[k]];
