@@ -321,10 +321,10 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
     s.cluster = c;
     s.threads = 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
-    // near window: 8 was the measured optimum on every skewed config (R-MAT-20
-    // 45.2 GTEPS at 8 vs 44.6 at the automatic 18; BA 30.4 at 8 vs 28.7 at 2;
-    // R-MAT-24 33.8 at 8 vs 32.9 at 19; weights up to 255)
-    if (!g->tune_near) s.near_width = 8;
+    // near window (weights up to 255): 8 for single-CTA teams (BA 31.6 vs 31.0
+    // at 12, 28.7 at 2), 12 for clusters (R-MAT-20 at C = 4: 50.4 vs 49.7 at 8,
+    // 50.2 at 16, 49.0 at 24; R-MAT-24: 35.3 vs 35.2 at 8, 34.8 at 16)
+    if (!g->tune_near) s.near_width = c >= 2 ? 12 : 8;
     return s;
   }
   // Flat, large graphs (grid / road-like: latency-bound rounds, small
