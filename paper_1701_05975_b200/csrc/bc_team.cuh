@@ -42,6 +42,16 @@
 
 #include "bc_kernels.cuh"
 
+#ifndef WBC_TEAM_REFILL_U
+#define WBC_TEAM_REFILL_U 4
+#endif
+#ifndef WBC_TEAM_SETTLE_U
+#define WBC_TEAM_SETTLE_U 2
+#endif
+#ifndef WBC_TEAM_BACK_U
+#define WBC_TEAM_BACK_U 4
+#endif
+
 namespace wbc_dev {
 
 struct TeamRed {
@@ -511,7 +521,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
         const uint32_t* src = fc ? fq1 : fq0;
         uint32_t* dst = fc ? fq0 : fq1;
         uint32_t* const nqc = nc ? nq1 : nq0;
-        constexpr int kRefillU = T <= 32 ? 8 : 4;  // far entries per lane per step
+        constexpr int kRefillU = T <= 32 ? 8 : WBC_TEAM_REFILL_U;  // far entries per lane per step
         for (uint32_t c = gtid; c < far_len; c += TT * kRefillU) {
           uint32_t u[kRefillU], du[kRefillU];
 #pragma unroll
@@ -564,7 +574,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
         // loads, distance and row-offset gathers of the step are in flight
         // together; a warp scan plus one packed atomic hands out (order
         // position, edge offset) for the settled lanes; no CTA barrier.
-        constexpr int kSettleU = T <= 32 ? 8 : 2;  // R-MAT-20: 2: 45.1, 4: 44.8, 8: 43.5 GTEPS
+        constexpr int kSettleU = T <= 32 ? 8 : WBC_TEAM_SETTLE_U;  // R-MAT-20 (C = 2): 2: 45.1, 4: 44.8, 8: 43.5 GTEPS
         const uint32_t lane = tid & 31;
         const uint32_t lt = (1u << lane) - 1u;
         for (uint32_t c = sb + (tid & ~31u) * kSettleU; c < se; c += T * kSettleU) {
@@ -727,7 +737,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
       for (uint32_t L = nlev - 1; L >= 1; --L) {
         // dag_ends[nlev] is written by the leader in this very phase: use the register
         const uint32_t b = __ldcg(dag_ends + L), e = L + 1 == nlev ? dag_len : __ldcg(dag_ends + L + 1);
-        constexpr int kBackU = 4;  // DAG edges per thread per step, loads in flight together
+        constexpr int kBackU = WBC_TEAM_BACK_U;  // DAG edges per thread per step, loads in flight together
         for (uint32_t c = b + gtid; c < e; c += TT * kBackU) {
           uint2 d[kBackU];
           uint32_t u[kBackU];
