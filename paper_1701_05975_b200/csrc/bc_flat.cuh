@@ -68,6 +68,10 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #ifndef WBC_FLAT_PREFETCH
 #define WBC_FLAT_PREFETCH 0
 #endif
+#ifndef WBC_FLAT_MEMD
+#define WBC_FLAT_MEMD 1
+#endif
+constexpr bool kSortKeepD = WBC_FLAT_MEMD;  // the window sort's counting pass parks each member's distance (coalesced) for the scatter pass
 constexpr bool kRelaxPrefetch = WBC_FLAT_PREFETCH;  // prefetch a pushed vertex's ELL row into L2
 #ifndef WBC_FLAT_SWEEPERS
 #define WBC_FLAT_SWEEPERS 1
@@ -185,9 +189,10 @@ __device__ __forceinline__ uint32_t* dist_of(uint2* dp, uint32_t v) { return rei
 // The whole KE = 4 record (slots and keys, 32 bytes) in one 256-bit load.
 __device__ __forceinline__ void ell_rec4(const FlatWs& w, uint32_t v, uint32_t (&r)[4], uint32_t (&k)[4]) {
   const uint32_t* p = w.ell + static_cast<uint64_t>(v) * 8;
-  uint32_t k01, k23, z0, z1;
-  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(k01), "=r"(k23), "=r"(z0), "=r"(z1)
+  uint32_t k01, k23;
+  asm("{.reg .b32 z0, z1;\n\t"
+      "ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,z0,z1}, [%6];}"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(k01), "=r"(k23)
       : "l"(p));
   k[0] = k01 & 0xFFFFu;
   k[1] = k01 >> 16;
@@ -564,7 +569,10 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
 #pragma unroll
           for (int j = 0; j < kM; ++j)
-            if (u[j] != kInfDist) atomicAdd(hist + (du[j] - lo), 1u);
+            if (u[j] != kInfDist) {
+              atomicAdd(hist + (du[j] - lo), 1u);
+              if constexpr (kSortKeepD) fq2[i0 + j * TG] = du[j];  // the far spare is free until the refill
+            }
         }
         gsync();
         // exclusive scan of hist[0, span): a contiguous chunk per thread
@@ -601,7 +609,8 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
           for (int j = 0; j < kM; ++j) u[j] = i0 + j * TG < mem_len ? mem[i0 + j * TG] : kInfDist;
 #pragma unroll
-          for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+          for (int j = 0; j < kM; ++j)
+            du[j] = u[j] == kInfDist ? 0u : kSortKeepD ? fq2[i0 + j * TG] : __ldcg(dist_of(dp, u[j]));
 #pragma unroll
           for (int j = 0; j < kM; ++j) {
             if (u[j] == kInfDist) continue;

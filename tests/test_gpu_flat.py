@@ -164,3 +164,34 @@ def test_flat_refuses_asymmetric_rows(W):
         assert gg.last_kernel().startswith("bc_flat_kernel")
     finally:
         gg.close()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_flat_random_sparse_graphs(W, oracle, seed):
+    """The flat kernel on random sparse graphs (not lattices): degree <= 8,
+    several components, weight ranges from ties-heavy to wide, both CTA
+    shapes; node / edge BC and depth against the oracle's Eq. 4."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(300, 900))
+    el = W.gen_er(n, float(rng.uniform(1.5, 3.5)), seed)
+    keep = np.ones(len(el), bool)
+    deg = np.zeros(n + 1, np.int64)
+    for i, (a, b) in enumerate(zip(el.u.tolist(), el.v.tolist())):  # cap the degree at 8
+        if deg[a] >= 8 or deg[b] >= 8:
+            keep[i] = False
+        else:
+            deg[a] += 1
+            deg[b] += 1
+    el = W.EdgeList(el.u[keep], el.v[keep], el.w[keep])
+    for lo, hi in ((1, 2), (1, 300)):
+        g = W.build_csr(W.assign_weights(el, lo, hi, seed))
+        for threads in (1024, 256):
+            gg = flat_graph(W, g)
+            try:
+                gg.set_param("flat_threads", threads)
+                check_graph(W, oracle, g, sources=W.sample_sources(g.n, 60, seed), edge=True, gg=gg)
+                assert gg.last_kernel().startswith("bc_flat_kernel")
+                assert gg.last_run_stats()["flat_fallback_sources"] == 0
+            finally:
+                gg.close()
+
