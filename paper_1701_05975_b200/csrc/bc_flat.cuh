@@ -71,6 +71,20 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #ifndef WBC_FLAT_MEMD
 #define WBC_FLAT_MEMD 1
 #endif
+#ifndef WBC_FLAT_L1
+#define WBC_FLAT_L1 14
+#endif
+// loads of data this CTA wrote (distances, positions, sigma, coef) through
+// L1 (ld.ca) instead of L2 only: bit 0 pass A distances, bit 1 pass B
+// neighbour words, bit 2 pass B predecessor sigma, bit 3 pass C coef
+constexpr int kFlatL1 = WBC_FLAT_L1;
+template <int BIT, class X>
+__device__ __forceinline__ X ld_own(const X* p) {
+  if constexpr (kFlatL1 >> BIT & 1)
+    return __ldca(p);
+  else
+    return __ldcg(p);
+}
 constexpr bool kSortKeepD = WBC_FLAT_MEMD;  // the window sort's counting pass parks each member's distance (coalesced) for the scatter pass
 constexpr bool kRelaxPrefetch = WBC_FLAT_PREFETCH;  // prefetch a pushed vertex's ELL row into L2
 #ifndef WBC_FLAT_SWEEPERS
@@ -496,7 +510,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           for (int j = 0; j < kRelaxU; ++j) {
             const uint32_t i = i0 + j * TG;
             const uint32_t v = i < near_len ? nq[i] : kInfDist;
-            dv[j] = v != kInfDist ? __ldcg(dist_of(dp, v)) : kInfDist;
+            dv[j] = v != kInfDist ? ld_own<0>(dist_of(dp, v)) : kInfDist;
             if (v != kInfDist)
               ell_row<KE>(w, v, r[j]);
             else
@@ -566,7 +580,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
           for (int j = 0; j < kM; ++j) u[j] = i0 + j * TG < mem_len ? mem[i0 + j * TG] : kInfDist;
 #pragma unroll
-          for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+          for (int j = 0; j < kM; ++j) du[j] = u[j] != kInfDist ? ld_own<0>(dist_of(dp, u[j])) : 0u;
 #pragma unroll
           for (int j = 0; j < kM; ++j)
             if (u[j] != kInfDist) {
@@ -637,7 +651,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
         for (int j = 0; j < kF; ++j) u[j] = i0 + j * TG < far_len ? fq[i0 + j * TG] : kInfDist;
 #pragma unroll
-        for (int j = 0; j < kF; ++j) du[j] = u[j] != kInfDist ? __ldcg(dist_of(dp, u[j])) : 0u;
+        for (int j = 0; j < kF; ++j) du[j] = u[j] != kInfDist ? ld_own<0>(dist_of(dp, u[j])) : 0u;
 #pragma unroll
         for (int j = 0; j < kF; ++j) {
           if (u[j] == kInfDist || du[j] < thr32) continue;  // joined an earlier window: sorted already
@@ -706,7 +720,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       for (int j = 0; j < kU; ++j)
 #pragma unroll
         for (int x = 0; x < KE; ++x)
-          nb[j][x] = (r[j][x] & wmask) ? __ldcg(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
+          nb[j][x] = (r[j][x] & wmask) ? ld_own<1>(dp + (r[j][x] >> wbits)) : make_uint2(kInfDist, 0u);
 #pragma unroll
       for (int j = 0; j < kU; ++j) {
         const uint32_t q = a + gt + j * TG;
@@ -740,7 +754,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
           for (int x = 0; x < KE; ++x)
             if (pm >> x & 1u) {
               if (sp[j][x] < a)
-                sg[j] += __ldcg(psig + sp[j][x]);
+                sg[j] += ld_own<2>(psig + sp[j][x]);
               else
                 pend[j] |= 1u << x;
             }
@@ -828,7 +842,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         for (int x = 0; x < KE; ++x) {
           if (!(sm[j] >> x & 1u)) continue;
           if (sp[j][x] >= bend) {
-            const double c = su[j] * __ldcg(pcoef + sp[j][x]);
+            const double c = su[j] * ld_own<3>(pcoef + sp[j][x]);
             dsum[j] += c;
             if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(w.ell_eid + static_cast<uint64_t>(u[j]) * KE + x), c);
           } else {

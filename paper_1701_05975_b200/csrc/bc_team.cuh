@@ -103,12 +103,33 @@ __device__ __forceinline__ uint32_t team_append(uint32_t* counter) {
 // relabel puts the most-gathered vertices first) carry the L2 evict-last
 // hint, the rest evict-normal; the policy is selected per access in a
 // register (no branch).  hot = n marks every entry.
+#ifndef WBC_TEAM_L1
+#define WBC_TEAM_L1 1
+#endif
+// Single-CTA teams own every word of their workspace, so reads of it may go
+// through L1 (ld.ca; coherent within the CTA after a barrier): bit 0 the
+// distances, bit 1 sigma / delta.  Clusters read words other SMs wrote: L2.
+template <int C, int BIT, class X>
+__device__ __forceinline__ X ld_team(const X* p) {
+  if constexpr (C == 1 && (WBC_TEAM_L1 >> BIT & 1))
+    return __ldca(p);
+  else
+    return __ldcg(p);
+}
+
 struct TeamDist {
   uint32_t* gl;
   uint64_t keep, norm;
   uint32_t hot;
   __device__ __forceinline__ uint64_t pol(uint32_t u) const { return u < hot ? keep : norm; }
   __device__ __forceinline__ uint32_t load(uint32_t u) const { return ld_cg_hint(gl + u, pol(u)); }
+  template <int C>
+  __device__ __forceinline__ uint32_t get(uint32_t u) const {
+    if constexpr (C == 1 && (WBC_TEAM_L1 & 1))
+      return __ldca(gl + u);
+    else
+      return load(u);
+  }
   __device__ __forceinline__ uint32_t fetch_min(uint32_t u, uint32_t v) const {
     return atom_min_hint(gl + u, v, pol(u));
   }
@@ -144,9 +165,12 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
 // Relax groups per warp step: 3 for clusters (R-MAT-20 at C = 4: 49.7 vs 48.6
 // GTEPS at 2, 48.7 at 4; R-MAT-24: 35.3 vs 35.0), 2 for single-CTA teams
 // (BA-65536: 31.7 vs 31.5 at 3).
+#ifndef WBC_TEAM_CUNROLL
+#define WBC_TEAM_CUNROLL 3
+#endif
 template <int T, int C>
-constexpr int team_unroll() { return (C >= 2 && T >= 1024) ? 3 : kUnroll; }
-constexpr uint32_t kTeamQ = 32 * 3 + 32;
+constexpr int team_unroll() { return (C >= 2 && T >= 1024) ? WBC_TEAM_CUNROLL : kUnroll; }
+constexpr uint32_t kTeamQ = 32 * (WBC_TEAM_CUNROLL > kUnroll ? WBC_TEAM_CUNROLL : kUnroll) + 32;
 __host__ __device__ constexpr size_t team_q_bytes(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
 template <int T>
 constexpr size_t team_sh_bytes() { return (sizeof(TeamShared<T>) + 15) / 16 * 16; }
@@ -379,7 +403,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
                   u = qpu[i];
                   v = qpv[i];
                   sl = qps[i];
-                  sg = __ldcg(sigma + u);
+                  sg = ld_team<C, 1>(sigma + u);
                 }
                 uint32_t base = 0;
                 if (lane == 0) base = atomicAdd(&R.dag_app, m);
@@ -439,7 +463,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
 #pragma unroll
                 for (int k = 0; k < kTU; ++k) {
                   const bool valid = e0 + 32 * k + lane < cwe;
-                  du[k] = valid ? dist.load(nbr(xw[k])) : 0u;
+                  du[k] = valid ? dist.template get<C>(nbr(xw[k])) : 0u;
                   cx[k] = xw[k];
                   cj[k] = jj[k];
                 }
@@ -530,7 +554,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             u[k] = i < far_len ? __ldcg(src + i) : 0u;
           }
 #pragma unroll
-          for (int k = 0; k < kRefillU; ++k) du[k] = c + k * TT < far_len ? dist.load(u[k]) : 0u;
+          for (int k = 0; k < kRefillU; ++k) du[k] = c + k * TT < far_len ? dist.template get<C>(u[k]) : 0u;
 #pragma unroll
           for (int k = 0; k < kRefillU; ++k) {
             if (c + k * TT < far_len && du[k] >= Fo) {  // du < Fo: already near or settled
@@ -587,7 +611,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             u[k] = have[k] ? __ldcg(src + i) : 0u;
           }
 #pragma unroll
-          for (int k = 0; k < kSettleU; ++k) du[k] = have[k] ? dist.load(u[k]) : kInfDist;
+          for (int k = 0; k < kSettleU; ++k) du[k] = have[k] ? dist.template get<C>(u[k]) : kInfDist;
 #pragma unroll
           for (int k = 0; k < kSettleU; ++k) {
             st[k] = have[k] && du[k] < thr;
@@ -701,7 +725,7 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
           const uint32_t w = has ? __ldcg(order + q) : 0u;
           const uint32_t dw = has ? __ldcg(ord_d + q) : 0u;
           const uint32_t rb = has ? __ldg(g.offsets + w) : 0u, re = has ? __ldg(g.offsets + w + 1) : 0u;
-          const double sw = has ? __ldcg(sigma + w) : 0.0;
+          const double sw = has ? ld_team<C, 1>(sigma + w) : 0.0;
           double part = 0.0;
           for (uint32_t st = 0; __any_sync(0xffffffffu, rb + st < re); st += G) {
             const uint32_t e = rb + st + gl;
@@ -710,12 +734,12 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             if (e < re) {
               uint32_t x, wt;
               load_slot<PACKED>(gr, e, x, wt);
-              const uint32_t dx = dist.load(x);
+              const uint32_t dx = dist.template get<C>(x);
               if (dx != kInfDist && dx == dw + wt) {
                 hit = true;
-                const double sx = __ldcg(sigma + x);
+                const double sx = ld_team<C, 1>(sigma + x);
                 note_sigma(p.overflow, sx);
-                c = __dmul_rn(__ddiv_rn(sw, sx), __dadd_rn(1.0, __ldcg(sdelta + x)));
+                c = __dmul_rn(__ddiv_rn(sw, sx), __dadd_rn(1.0, ld_team<C, 1>(sdelta + x)));
                 if (eacc) eacc[__ldg(p.ref_edge_id + e)] = c;
               }
             }
@@ -754,9 +778,9 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
             if (c + k * TT >= e) continue;
             const uint32_t v = d[k].y;
             // reference term: sw / sigma[v] * (1.0 + delta[v])  (engine.cpp:201)
-            const double sv = __ldcg(sigma + v);
+            const double sv = ld_team<C, 1>(sigma + v);
             note_sigma(p.overflow, sv);
-            const double cc = __ldcg(sigma + u[k]) / sv * (1.0 + __ldcg(delta + v));
+            const double cc = ld_team<C, 1>(sigma + u[k]) / sv * (1.0 + ld_team<C, 1>(delta + v));
             atomicAdd(delta + u[k], cc);
             if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + d[k].x), cc);
           }
@@ -791,12 +815,12 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
               const uint32_t slot = sh.rowadj[jl] + e;
               uint32_t x, w;
               load_slot<PACKED>(g, slot, x, w);
-              const uint32_t dx = dist.load(x);
+              const uint32_t dx = dist.template get<C>(x);
               if (dx != kInfDist && dx == sh.dv[jl] + w) {
                 const uint32_t wv = sh.v[jl];
-                const double sx = __ldcg(sigma + x);
+                const double sx = ld_team<C, 1>(sigma + x);
                 note_sigma(p.overflow, sx);
-                const double c2 = __ldcg(sigma + wv) / sx * (1.0 + __ldcg(delta + x));
+                const double c2 = ld_team<C, 1>(sigma + wv) / sx * (1.0 + ld_team<C, 1>(delta + x));
                 atomicAdd(&sh.acc[jl], c2);
                 if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + slot), c2);
               }
