@@ -84,7 +84,6 @@ struct TeamShared {
   uint32_t dv[CH];
   uint32_t rowadj[CH];  // row start + chunk base - first edge (mod 2^32)
   uint32_t pref[CH + 1];
-  double acc[CH];
   TeamRed ring[4];     // used through rank 0's copy
   uint32_t bcast;
   unsigned long long src_idx;  // launch-relative index of the current source (strict merge)
@@ -176,8 +175,11 @@ template <int T>
 constexpr size_t team_sh_bytes() { return (sizeof(TeamShared<T>) + 15) / 16 * 16; }
 // Dynamic shared memory of a team CTA: the staged chunk + phase ring, then the
 // per-warp queues.
+#ifndef WBC_TEAM_SMEM_PAD
+#define WBC_TEAM_SMEM_PAD 0
+#endif
 inline size_t team_dyn_smem(int threads) {
-  return threads <= 32 ? team_sh_bytes<32>() + team_q_bytes(32) : team_sh_bytes<1024>() + team_q_bytes(1024);
+  return threads <= 32 ? team_sh_bytes<32>() + team_q_bytes(32) : team_sh_bytes<1024>() + team_q_bytes(1024) + WBC_TEAM_SMEM_PAD;
 }
 
 // 1024-thread CTAs: one per SM.  32-thread CTAs (one warp per source, for
@@ -278,7 +280,6 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
         sh.dv[t] = od[r];
         sh.rowadj[t] = orow[r] + cb - gs[r];
         sh.pref[t] = (gs[r] > cb ? gs[r] : cb) - cb;
-        sh.acc[t] = 0.0;
       }
     }
     if (tid == T - 1) sh.bcast = nxt;
@@ -798,6 +799,13 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
       // buffer overflowed: phase L computes delta of level L from its rows
       // and adds the (final) delta of level L+1 to node BC.
       if (leader) atomicAdd(p.overflow, 1u);
+      // per-chunk delta sums live in the (now idle) relax queues: keeping
+      // them out of TeamShared keeps the CTA's shared memory within the
+      // 100 KB carveout, which leaves L1 156 KB instead of 124 KB
+      static_assert(team_q_bytes(T) >= CH * sizeof(double), "acc fits the queue region");
+      double* const acc = reinterpret_cast<double*>(team_q);
+      for (int t = tid; t < CH; t += T) acc[t] = 0.0;
+      __syncthreads();
       for (int L = static_cast<int>(nlev) - 1; L >= 0; --L) {
         const uint32_t pb = __ldcg(lev + L), pe = static_cast<uint32_t>(L) + 1 == nlev ? ord_len : __ldcg(lev + L + 1);
         const uint32_t lEb = __ldcg(epref + pb);
@@ -821,13 +829,16 @@ __global__ void __launch_bounds__(T, team_min_blocks(T)) bc_team_kernel(const Ru
                 const double sx = ld_team<C, 1>(sigma + x);
                 note_sigma(p.overflow, sx);
                 const double c2 = ld_team<C, 1>(sigma + wv) / sx * (1.0 + ld_team<C, 1>(delta + x));
-                atomicAdd(&sh.acc[jl], c2);
+                atomicAdd(&acc[jl], c2);
                 if (p.edge_bc) atomicAdd(p.edge_bc + __ldg(g.edge_id + slot), c2);
               }
             });
             __syncthreads();
             for (int t = tid; t < cnt; t += T)
-              if (sh.acc[t] != 0.0) atomicAdd(delta + sh.v[t], sh.acc[t]);
+              if (acc[t] != 0.0) {
+                atomicAdd(delta + sh.v[t], acc[t]);
+                acc[t] = 0.0;
+              }
             __syncthreads();
             j += cnt;
             cb = ce;
