@@ -16,6 +16,7 @@ O = Oracle()
 tol = lambda a, b: np.abs(a - b) <= np.maximum(1e-12, 1e-9 * np.maximum(np.abs(a), np.abs(b)))  # noqa: E731
 kron = W.build_csr(W.assign_weights(W.gen_kronecker(11, 16.0, 3), 1, 255, 3))
 grid = W.build_csr(W.assign_weights(W.gen_grid(24, 24), 1, 1000, 3))
+bip = W.build_csr(W.EdgeList.of([(i, 60 + j, 1.0) for i in range(60) for j in range(60)]))  # DAG > buffer: row-scan fallback
 cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("team C=1", kron, {"cluster": 1}),
          ("team C=2", kron, {"cluster": 2}),
@@ -26,7 +27,9 @@ cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("flat kernel, 256 threads", grid, {"flat": 1, "flat_threads": 256, "slots": 2}),
          ("flat kernel, long distances", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
          ("flat kernel, unit weights", W.build_csr(W.assign_weights(W.gen_grid(12, 10), 1, 1, 3)), {"flat": 1}),
-         ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8})]
+         ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8}),
+         ("team C=1, DAG overflow", bip, {"cluster": 1}),
+         ("team C=4, DAG overflow", bip, {"cluster": 4})]
 for name, g, params in cases:
     src = W.sample_sources(g.n, 12 if params.get("flat") else 6, 1)  # flat: more sources than CTAs cycle the sweep buffers
     gg = W.GpuGraph(g, 0)
