@@ -216,6 +216,11 @@ KernelFn pick_team_t(int c, int threads) {
     case 2: return bc_team_kernel<1024, 2, PACKED, PROF>;
     case 4: return bc_team_kernel<1024, 4, PACKED, PROF>;
     case 8: return bc_team_kernel<1024, 8, PACKED, PROF>;
+#ifdef WBC_TEAM_ODD_CLUSTERS
+    case 6: return bc_team_kernel<1024, 6, PACKED, PROF>;
+    case 9: return bc_team_kernel<1024, 9, PACKED, PROF>;
+    case 12: return bc_team_kernel<1024, 12, PACKED, PROF>;
+#endif
     default: return bc_team_kernel<1024, 16, PACKED, PROF>;
   }
 }
@@ -300,6 +305,9 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
   if (g->tune_cluster > 0) {
     s.cluster = g->tune_cluster <= 1 ? 1 : g->tune_cluster <= 2 ? 2 : g->tune_cluster <= 4 ? 4
               : g->tune_cluster <= 8 ? 8 : 16;
+#ifdef WBC_TEAM_ODD_CLUSTERS
+    if (g->tune_cluster == 6 || g->tune_cluster == 9 || g->tune_cluster == 12) s.cluster = g->tune_cluster;
+#endif
     s.threads = (s.cluster == 1 && g->tune_threads > 0 && g->tune_threads <= 32) ? 32 : 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
     return s;
