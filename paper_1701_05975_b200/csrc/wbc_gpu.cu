@@ -329,10 +329,11 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
     s.cluster = c;
     s.threads = 1024;
     s.dyn_smem = wbc_dev::team_dyn_smem(s.threads);
-    // near window (weights up to 255): 8 for single-CTA teams (BA 31.6 vs 31.0
-    // at 12, 28.7 at 2), 12 for clusters (R-MAT-20 at C = 4: 50.4 vs 49.7 at 8,
-    // 50.2 at 16, 49.0 at 24; R-MAT-24: 35.3 vs 35.2 at 8, 34.8 at 16)
-    if (!g->tune_near) s.near_width = c >= 2 ? 12 : 8;
+    // near window (weights up to 255): 6 for single-CTA teams (BA 33.0 vs 32.8
+    // at 8, 32.5 at 10, 32.2 at 12, 28.7 at 2), 12 for clusters (R-MAT-20 at
+    // C = 4: 51.4 vs 51.1-51.3 at 10-16, 50.5 at 20; R-MAT-24: 35.3 vs 35.2 at
+    // 8, 34.8 at 16)
+    if (!g->tune_near) s.near_width = c >= 2 ? 12 : 6;
     return s;
   }
   // Flat, large graphs (grid / road-like: latency-bound rounds, small

@@ -12,8 +12,13 @@ ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("shapes", nargs="+")
 a = ap.parse_args()
 t = time.time()
-scale = int(a.graph[4:])
-g = W.build_csr(W.assign_weights(W.gen_kronecker(scale, 32.0, 1), 1, 255, 1))
+if a.graph == "ba":
+    g = W.build_csr(W.assign_weights(W.gen_ba(65536, 10, 1), 1, 100, 1))
+elif a.graph.startswith("grid"):
+    s_ = int(a.graph[4:])
+    g = W.build_csr(W.assign_weights(W.gen_grid(s_, s_), 1, 1000, 1))
+else:
+    g = W.build_csr(W.assign_weights(W.gen_kronecker(int(a.graph[4:]), 32.0, 1), 1, 255, 1))
 print(f"graph {a.graph} n={g.n} m={g.m} built in {time.time()-t:.1f}s", flush=True)
 src = W.sample_sources(g.n, a.k, 1)
 for rnd in range(2):
