@@ -25,6 +25,8 @@ for rnd in range(2):
     for sh in a.shapes:
         gg = W.GpuGraph(g, 0)
         for kv in sh.split(","):
+            if kv == "default":
+                continue
             k_, v_ = kv.split("=")
             gg.set_param(k_, int(v_))
         best = 0.0
