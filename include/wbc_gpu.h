@@ -143,7 +143,9 @@ int wbc_gpu_set_tuning(wbc_gpu_graph* g, int threads_per_cta, int max_slots,
  * most k - 1 fill teams),
  * "flat" (distance-first kernel for flat graphs: -1 auto = degree <= 8 and
  * n >= 2^18, 0 off, 1 wherever eligible), "flat_delta" (its near-far window;
- * 0 = max weight), "flat_threads" (its CTA size: 256, 512 or 1024).  Unknown
+ * 0 = max weight), "flat_threads" (its CTA size: 256, 512 or 1024),
+ * "flat_sq" (its shared-memory near-queue entries per buffer; -1 = auto:
+ * what fits below the 64 KB carveout step, 0 = global-memory queues only).  Unknown
  * names return WBC_E_INVALID. */
 int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value);
 

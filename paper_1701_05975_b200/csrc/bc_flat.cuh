@@ -68,6 +68,11 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #ifndef WBC_FLAT_PREFETCH
 #define WBC_FLAT_PREFETCH 0
 #endif
+#ifndef WBC_FLAT_SQ
+#define WBC_FLAT_SQ 4096
+#endif
+constexpr size_t kFlatSQ = WBC_FLAT_SQ;             // cap of the shared-memory near-queue entries per buffer
+constexpr size_t kFlatSmemStep = 64 * 1024;         // the carveout step the kernel's other shared memory fits in
 #ifndef WBC_FLAT_MEMD
 #define WBC_FLAT_MEMD 1
 #endif
@@ -116,6 +121,7 @@ struct FlatWs {
   uint32_t delta_w;         // window width (<= kFlatBuckets)
   uint32_t buckets;         // power of two >= maxw + max minw + 2
   uint32_t delta_words;     // shared-memory words of the window-sort histogram (>= delta_w)
+  uint32_t sq_cap;          // near-queue entries per buffer kept in shared memory (the rest spill to q0 / q1)
 };
 
 __device__ __forceinline__ double ld_relaxed_f64(const double* a) {
@@ -158,6 +164,11 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // Dynamic shared memory of bc_flat_kernel<T, KE>: the workers' window-sort
 // histogram, then per sweeper its bucket ring and cp.async ring.
+// static shared memory of bc_flat_kernel<T, *> (s_blk dominates), rounded up
+inline size_t flat_static_smem(int threads) {
+  return static_cast<size_t>(threads - 32 * kSweepers) * 2 * 8 + threads / 8 + 1024;
+}
+// without the near queues (the host adds 2 * sq_cap words)
 inline size_t flat_dyn_smem(uint32_t delta_words, uint32_t buckets, int ke) {
   return (static_cast<size_t>(delta_words) +
           kSweepers * (buckets + static_cast<size_t>(kFlatRing) * kFlatChunk * (1 + ke))) * 4;
@@ -384,7 +395,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
   __shared__ uint32_t s_warp[T / 32];
   __shared__ double s_blk[kBlk];             // the block's sigma (B) / coef (C); 0 = not final
   __shared__ uint32_t s_sw[kSW][2][3];       // per sweeper and buffer: reached, source, exit
-  extern __shared__ uint32_t smem[];         // hist | buckets | sweep ring
+  extern __shared__ uint32_t smem[];         // hist | per sweeper: buckets, sweep ring | near queues
   const GraphView& g = p.g;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31, wid = tid >> 5;
@@ -397,6 +408,10 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
   uint32_t* const pinfo = w.pinfo + off;
   uint32_t* const psucc = w.psucc + off * KE;
   uint32_t* const hist = smem;
+  // near queues: entries [0, sq_cap) in shared memory, the rest in q0 / q1
+  uint32_t* const sq0 = smem + w.delta_words + kSW * (w.buckets + kFlatRing * kFlatChunk * (1 + KE));
+  uint32_t* const sq1 = sq0 + w.sq_cap;
+  const uint32_t sqc = w.sq_cap;
   const uint32_t wbits = g.wbits, wmask = g.wmask;
   // the sweep inputs are double-buffered per sweeper: buffer (j, parity)
   auto ord_d_of = [&](uint32_t j, uint32_t par) { return w.ord_d + (2 * kSW * off + (2 * j + par) * w.n_stride); };
@@ -478,7 +493,10 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     gsync();
     if (gt == 0) {
       *dist_of(dp, s) = 0;
-      w.q0[off] = s;
+      if (sqc)
+        sq0[0] = s;
+      else
+        w.q0[off] = s;
       mem[0] = s;
     }
     gsync();
@@ -487,6 +505,8 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
     // ---- A. near-far SSSP; windows sorted into `order` as they close
     uint32_t* nq = w.q0 + off;
     uint32_t* nn = w.q1 + off;
+    uint32_t* snq = sq0;
+    uint32_t* snn = sq1;
     uint32_t* fq = w.q2 + off;
     uint32_t* fq2 = w.q3 + off;
     uint32_t near_len = 1, far_len = 0, mem_len = 1, olen = 0, ph = 0, windows = 0;
@@ -509,7 +529,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
 #pragma unroll
           for (int j = 0; j < kRelaxU; ++j) {
             const uint32_t i = i0 + j * TG;
-            const uint32_t v = i < near_len ? nq[i] : kInfDist;
+            const uint32_t v = i < near_len ? (i < sqc ? snq[i] : nq[i]) : kInfDist;
             dv[j] = v != kInfDist ? ld_own<0>(dist_of(dp, v)) : kInfDist;
             if (v != kInfDist)
               ell_row<KE>(w, v, r[j]);
@@ -546,7 +566,11 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
                 // duplicates in the next near list are harmless (a re-relax
                 // reads the current distance); members are appended once, at
                 // the crossing below the window end
-                nn[atomicAdd(&R[0], 1u)] = u;
+                const uint32_t k = atomicAdd(&R[0], 1u);
+                if (k < sqc)
+                  snn[k] = u;
+                else
+                  nn[k] = u;
                 if constexpr (kRelaxPrefetch) asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_rec<KE>(w, u)));
                 if (old[j][x] >= thr32) mem[mem_len + atomicAdd(&R[2], 1u)] = u;
               } else if (old[j][x] == kInfDist) {
@@ -564,6 +588,9 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         uint32_t* t = nq;
         nq = nn;
         nn = t;
+        t = snq;
+        snq = snn;
+        snn = t;
         ++ph;
         continue;
       }
@@ -656,7 +683,11 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         for (int j = 0; j < kF; ++j) {
           if (u[j] == kInfDist || du[j] < thr32) continue;  // joined an earlier window: sorted already
           if (du[j] < tn32) {
-            nq[atomicAdd(&R[0], 1u)] = u[j];
+            const uint32_t k = atomicAdd(&R[0], 1u);
+            if (k < sqc)
+              snq[k] = u[j];
+            else
+              nq[k] = u[j];
             if constexpr (kRelaxPrefetch) asm volatile("prefetch.global.L2 [%0];" ::"l"(ell_rec<KE>(w, u[j])));
             mem[atomicAdd(&R[2], 1u)] = u[j];
           } else {

@@ -92,6 +92,7 @@ struct LaunchShape {
   uint32_t hot = 0;        // vertices with shared-memory distances
   uint32_t l2hot = 0;      // vertices whose distance accesses carry an evict-last hint
   size_t dyn_smem = 0;     // bytes
+  uint32_t flat_sq = 0;    // flat kernel: shared-memory near-queue entries per buffer
 };
 
 struct wbc_gpu_graph {
@@ -163,6 +164,7 @@ struct wbc_gpu_graph {
   int tune_flat = -1;          // -1 auto (flat, large graphs), 0 off, 1 wherever eligible
   uint32_t tune_flat_delta = 0;  // near-far window of bc_flat_kernel (0: max weight)
   int tune_flat_threads = 0;     // bc_flat_kernel CTA size (0: kFlatT)
+  int tune_flat_sq = -1;         // bc_flat_kernel shared-memory near-queue entries per buffer (-1: auto)
   uint32_t max_degree = 0, max_minw = 0;
   bool symmetric = false;
   int scale_k = 0;             // weights scaled by 2^scale_k to integers (dumps scale distances back)
@@ -298,6 +300,14 @@ LaunchShape pick_shape_uncached(const wbc_gpu_graph* g) {
     s.threads = g->tune_flat_threads ? (g->tune_flat_threads <= 256 ? 256 : g->tune_flat_threads <= 512 ? 512 : 1024)
                                      : kFlatT;
     s.dyn_smem = wbc_dev::flat_dyn_smem(flat_delta_words(g), flat_buckets(g), g->flat_ke);
+    // the near queues' first entries live in shared memory (two buffers),
+    // sized to the room left below the 64 KB carveout step: more shared
+    // memory would shrink L1, which the kernel needs more
+    const size_t used = s.dyn_smem + wbc_dev::flat_static_smem(s.threads) + 1024;
+    const size_t room = used < wbc_dev::kFlatSmemStep ? (wbc_dev::kFlatSmemStep - used) / 8 : 0;
+    const size_t want = g->tune_flat_sq >= 0 ? static_cast<size_t>(g->tune_flat_sq) : wbc_dev::kFlatSQ;
+    s.flat_sq = static_cast<uint32_t>(std::min(want, g->tune_flat_sq >= 0 ? want : room) / 32 * 32);
+    s.dyn_smem += size_t{2} * s.flat_sq * 4;
     return s;
   }
   const uint64_t n = g->n;
@@ -479,7 +489,7 @@ int ensure_bytes(wbc_gpu_graph* g, uint64_t bytes) {
 // Ensure a workspace for `want` slots exists (shape-dependent occupancy).
 int ensure_workspace(wbc_gpu_graph* g, int want, const LaunchShape& shape, int* slots_out) {
   // same knobs, same request, layout still carved: nothing to query or carve
-  const int shape_key = shape.cluster * 8192 + shape.threads * 4 + (shape.flat ? 2 : 0);
+  const int shape_key = shape.cluster * 8192 + shape.threads * 4 + (shape.flat ? 2 : 0) + static_cast<int>(shape.flat_sq) * 65536;
   if (g->d_ws && g->ws_gen == g->tune_gen && g->ws_want == want && g->ws_shape_key == shape_key) {
     *slots_out = g->ws_slots_cached;
     return WBC_OK;
@@ -672,7 +682,9 @@ int launch_run(wbc_gpu_graph* g, const uint32_t* d_sources, uint64_t k, bool edg
     rc = launch_strict(g, shape, slots, p, k, edge_bc, d_edge, strict_lanes, stream);
     if (rc) return rc;
   } else if (shape.flat) {
-    pick_flat(shape.threads, g->flat_ke)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p, g->fw);
+    wbc_dev::FlatWs fw = g->fw;
+    fw.sq_cap = shape.flat_sq;
+    pick_flat(shape.threads, g->flat_ke)<<<slots, shape.threads, shape.dyn_smem, stream>>>(p, fw);
     WBC_CUDA_TRY(cudaGetLastError());
   } else if (shape.cluster > 0) {
     // whole distance arrays of the few in-flight teams get evict-last
@@ -1232,6 +1244,7 @@ int wbc_gpu_set_param(wbc_gpu_graph* g, const char* name, int64_t value) {
   else if (k == "flat") g->tune_flat = static_cast<int>(value);
   else if (k == "flat_delta") g->tune_flat_delta = static_cast<uint32_t>(std::max<int64_t>(0, value));
   else if (k == "flat_threads") g->tune_flat_threads = static_cast<int>(value);
+  else if (k == "flat_sq") g->tune_flat_sq = static_cast<int>(std::max<int64_t>(-1, std::min<int64_t>(value, 1 << 14)));
   else return set_error(WBC_E_INVALID, "unknown tuning parameter '" + k + "'");
   return WBC_OK;
 }

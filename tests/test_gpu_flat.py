@@ -195,3 +195,18 @@ def test_flat_random_sparse_graphs(W, oracle, seed):
             finally:
                 gg.close()
 
+
+
+@pytest.mark.parametrize("sq", [0, 32])
+def test_flat_near_queue_spill(W, oracle, sq):
+    """Near queues entirely in global memory (flat_sq 0) and a 32-entry
+    shared-memory part that most phases overflow into q0 / q1."""
+    for name, g in _cases(W):
+        gg = flat_graph(W, g)
+        try:
+            gg.set_param("flat_sq", sq)
+            src = None if g.n <= 64 else W.sample_sources(g.n, 32, 5)
+            check_graph(W, oracle, g, sources=src, edge=True, gg=gg)
+            assert gg.last_kernel().startswith("bc_flat_kernel"), name
+        finally:
+            gg.close()
