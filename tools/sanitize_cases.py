@@ -25,6 +25,7 @@ cases = [("per-CTA kernel (tiny graph)", kron, {}),
          ("team C=4 + 2-CTA fill", kron, {"cluster": 4, "fill": 1}),
          ("flat kernel, 1024 threads", grid, {"flat": 1, "slots": 3}),
          ("flat kernel, 256 threads", grid, {"flat": 1, "flat_threads": 256, "slots": 2}),
+         ("flat kernel, near queues spilling", grid, {"flat": 1, "flat_sq": 32, "slots": 3}),
          ("flat kernel, long distances", W.build_csr(W.assign_weights(W.gen_grid(6, 6), 200, 1000, 3)), {"flat": 1}),
          ("flat kernel, unit weights", W.build_csr(W.assign_weights(W.gen_grid(12, 10), 1, 1, 3)), {"flat": 1}),
          ("strict merge (team C=2)", kron, {"cluster": 2, "_strict": 8}),
