@@ -161,14 +161,14 @@ __device__ __forceinline__ uint32_t block_find(const uint32_t* key, uint32_t lo,
 // Per-warp compaction queues of the two-pass relax (dynamic shared memory):
 // 5 arrays of kTeamQ u32 per warp; a warp holds < 32 entries between drains
 // and adds at most 32 * team_unroll per step.
-// Relax groups per warp step: 3 for clusters (R-MAT-20 at C = 4: 49.7 vs 48.6
-// GTEPS at 2, 48.7 at 4; R-MAT-24: 35.3 vs 35.0), 2 for single-CTA teams
-// (BA-65536: 31.7 vs 31.5 at 3).
+// Relax groups per warp step: 3 for 1024-thread teams (R-MAT-20 at C = 4:
+// 50.7 vs 48.6 GTEPS at 2, 48.7 at 4; R-MAT-24: 35.3 vs 35.0; BA-65536 at
+// C = 1: 33.2 vs 32.7 at 2, 30.0 at 1), kUnroll for one-warp teams.
 #ifndef WBC_TEAM_CUNROLL
 #define WBC_TEAM_CUNROLL 3
 #endif
 template <int T, int C>
-constexpr int team_unroll() { return (C >= 2 && T >= 1024) ? WBC_TEAM_CUNROLL : kUnroll; }
+constexpr int team_unroll() { return T >= 1024 ? WBC_TEAM_CUNROLL : kUnroll; }
 constexpr uint32_t kTeamQ = 32 * (WBC_TEAM_CUNROLL > kUnroll ? WBC_TEAM_CUNROLL : kUnroll) + 32;
 __host__ __device__ constexpr size_t team_q_bytes(int threads) { return size_t(threads / 32) * 5 * kTeamQ * 4; }
 template <int T>
