@@ -46,6 +46,11 @@ constexpr uint32_t kInfDist = 0xFFFFFFFFu;
 #define WBC_TEAM_UNROLL 2
 #endif
 constexpr int kUnroll = WBC_TEAM_UNROLL;  // 32-edge groups per warp step in relax (R-MAT-20 at C=2: 1: 38.2, 2: 44.8, 3: 44.4, 4: 43.9, 6: 32.3, 8: 17.3 GTEPS)
+#ifndef WBC_SRC_UNROLL
+#define WBC_SRC_UNROLL 1
+#endif
+// the same, in bc_sources_kernel (ER-4096: 1: 16.9, 2: 16.65, 3: 16.3, 4: 15.25 GTEPS)
+constexpr int kSrcUnroll = WBC_SRC_UNROLL;
 
 // ---- L2 residency hints.  The CSR slot stream (read once per source, 4 B
 // per slot, far larger than L2) is marked evict-first and skips L1; the
@@ -448,26 +453,26 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1536 / T)) bc_sources_kern
         uint32_t wb, we;
         if (warp_range<T>(total, wb, we)) {
           int j0 = find_row(sh.pref, cnt, wb);
-          // kUnroll independent slot -> dist chains per lane: all slot loads,
+          // kSrcUnroll independent slot -> dist chains per lane: all slot loads,
           // then all distance loads, then the compare / atomic / append work.
-          for (uint32_t e0 = wb; e0 < we; e0 += 32 * kUnroll) {
-            int jj[kUnroll];
-            uint32_t slot[kUnroll], uu[kUnroll], ww[kUnroll], du[kUnroll];
+          for (uint32_t e0 = wb; e0 < we; e0 += 32 * kSrcUnroll) {
+            int jj[kSrcUnroll];
+            uint32_t slot[kSrcUnroll], uu[kSrcUnroll], ww[kSrcUnroll], du[kSrcUnroll];
 #pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
+            for (int k = 0; k < kSrcUnroll; ++k) {
               const uint32_t eg = e0 + 32 * k;
               jj[k] = eg < we ? group_row(sh.pref, cnt, eg, j0) : 0;
               const uint32_t e = eg + (tid & 31);
               slot[k] = e < we ? sh.row[jj[k]] + (e - sh.pref[jj[k]]) : 0xFFFFFFFFu;
             }
 #pragma unroll
-            for (int k = 0; k < kUnroll; ++k)
+            for (int k = 0; k < kSrcUnroll; ++k)
               if (slot[k] != 0xFFFFFFFFu) load_slot<PACKED>(g, slot[k], uu[k], ww[k], stream_pol);
 #pragma unroll
-            for (int k = 0; k < kUnroll; ++k)
+            for (int k = 0; k < kSrcUnroll; ++k)
               if (slot[k] != 0xFFFFFFFFu) du[k] = dist.load(uu[k]);
 #pragma unroll
-            for (int k = 0; k < kUnroll; ++k) {
+            for (int k = 0; k < kSrcUnroll; ++k) {
               if (slot[k] == 0xFFFFFFFFu) continue;
               const int j = jj[k];
               const uint32_t u = uu[k], w = ww[k];
