@@ -68,6 +68,9 @@ constexpr int kFlatRing = 4;          // sweep ring: chunks (kFlatRing - 1 in fl
 #ifndef WBC_FLAT_PREFETCH
 #define WBC_FLAT_PREFETCH 0
 #endif
+#ifndef WBC_FLAT_SORT_U
+#define WBC_FLAT_SORT_U 4  // window-sort members / far entries per thread and step
+#endif
 #ifndef WBC_FLAT_KU
 #define WBC_FLAT_KU 2
 #endif
@@ -80,7 +83,7 @@ constexpr size_t kFlatSmemStep = 64 * 1024;         // the carveout step the ker
 #define WBC_FLAT_MEMD 1
 #endif
 #ifndef WBC_FLAT_L1
-#define WBC_FLAT_L1 14
+#define WBC_FLAT_L1 15
 #endif
 // loads of data this CTA wrote (distances, positions, sigma, coef) through
 // L1 (ld.ca) instead of L2 only: bit 0 pass A distances, bit 1 pass B
@@ -604,7 +607,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
         const uint32_t span = static_cast<uint32_t>(thr - lo < w.delta_w ? thr - lo : w.delta_w);
         for (uint32_t i = gt; i < span; i += TG) hist[i] = 0;
         gsync();
-        constexpr int kM = 4;  // members per thread and step, gathers in flight together
+        constexpr int kM = WBC_FLAT_SORT_U;  // members per thread and step, gathers in flight together
         for (uint32_t i0 = gt; i0 < mem_len; i0 += TG * kM) {
           uint32_t u[kM], du[kM];
 #pragma unroll
@@ -675,7 +678,7 @@ __global__ void __launch_bounds__(T, 1024 / T) bc_flat_kernel(const RunParams p,
       // (and members); the rest are compacted into the other far buffer
       const uint64_t thr_new = thr + w.delta_w;
       const uint32_t tn32 = thr_new >= kInfDist ? kInfDist : static_cast<uint32_t>(thr_new);
-      constexpr int kF = 4;  // far entries per thread and step, gathers in flight together
+      constexpr int kF = WBC_FLAT_SORT_U;  // far entries per thread and step, gathers in flight together
       for (uint32_t i0 = gt; i0 < far_len; i0 += TG * kF) {
         uint32_t u[kF], du[kF];
 #pragma unroll
