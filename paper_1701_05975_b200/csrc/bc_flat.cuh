@@ -27,26 +27,32 @@
 //      the far refill).  When a window closes its members are final; a
 //      shared-memory counting sort on d - lo appends them to `order` /
 //      `ord_d` and writes each one's position into its word, so the whole
-//      source ends up sorted by distance with no pass over n.
-//   B. sigma, pulled in distance order (thread per position): a vertex sums
-//      sigma over its DAG predecessors (d(u) + w == d(v)), all at earlier
-//      positions, waiting on each until it is nonzero (sigma >= 1 once
-//      written: the value is its own completion flag).  Integer-valued fp64,
-//      exact in any order below 2^53 (engine.cpp:73-77).  The same pass
-//      writes, per position, the successor mask and successor positions, and
-//      the threshold-sweep entries of every slot to a farther neighbour
-//      (w + minw(v), d(v) - d(u)), all coalesced.
-//   C. delta, pulled in reverse distance order by all warps but warp 0:
+//      source ends up sorted by distance with no pass over n.  The near
+//      queues' first sq_cap entries live in shared memory.
+//   B. sigma, pulled in distance order, a block of kBlk positions at a time
+//      (kU per worker thread): predecessors (d(u) + w == d(v)) in earlier
+//      blocks are final in `psig`; those inside the block resolve in barrier
+//      rounds over the block's shared-memory copy (read, barrier, publish;
+//      sigma >= 1, so 0 means not yet final).  Integer-valued fp64, exact in
+//      any order below 2^53 (engine.cpp:73-77).  The same pass writes, per
+//      position, the successor mask and positions and the threshold-sweep
+//      entries of every slot to a farther neighbour (w + minw(v),
+//      d(v) - d(u)), all coalesced.
+//   C. delta, pulled in reverse distance order the same way:
 //      c = sigma(u) * coef(v) over DAG successors v, where
-//      coef(v) = (1 + delta(v)) / sigma(v) is written once v is final
-//      (positive: its own completion flag); the reference's term is
-//      sigma[u] / sigma[v] * (1 + delta[v]) (engine.cpp:201), equal up to
-//      fp64 rounding.  Node BC += delta (u != s), edge BC += c.
-//      Concurrently warp 0 sweeps the Eq. 4 thresholds: a shared-memory
-//      bucket ring keyed by d(u) + w + minw(v) holds the largest successor
-//      distance + 1 (a key is live while that is above the threshold); the
-//      sorted distances and entries stream through a cp.async ring of
-//      shared-memory chunks, so a round costs shared-memory work only.
+//      coef(v) = (1 + delta(v)) / sigma(v) (positive: its own completion
+//      flag); the reference's term is sigma[u] / sigma[v] * (1 + delta[v])
+//      (engine.cpp:201), equal up to fp64 rounding.  Node BC += delta
+//      (u != s), edge BC += c.
+// A dedicated sweeper warp runs the Eq. 4 threshold sweep of the previous
+// source while the workers run A/B/C of the next (its sorted distances and
+// entries are double-buffered): a shared-memory bucket ring keyed by
+// d(u) + w + minw(v) holds the largest successor distance + 1 (a key is live
+// while that is above the threshold); positions stream through a cp.async
+// ring, so a level costs shared-memory work only.
+// Everything a CTA gathers in B and C (and its own distances in A) it wrote
+// itself: those loads go through L1 (ld.ca, coherent within the CTA after a
+// barrier), which on this kernel is worth more than any further shared memory.
 // No source is ever handed back: the window sort's range is delta_w, not the
 // distance range.
 #pragma once
